@@ -1,0 +1,196 @@
+/*
+ * bd_b200.h -- C ABI of the B200-native Brownian-dynamics hot path.
+ *
+ * Drop-in boundary for the per-timestep path of the reference package
+ * `brownsim` (arXiv 1703.02484 re-implementation, /root/reference/pkg).  The
+ * reference has no formal plugin registry; its two de-facto boundaries are
+ * (i) the kernel module brownsim._kernels (numpy arrays in, new arrays +
+ * `err` sentinels out) and (ii) the simulation classes' step()/run().  Each
+ * entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer (cudaMalloc / torch CUDA storage)
+ *     unless the name says _host; layouts are the reference's numpy layouts
+ *     (positions (N,2) float64 row-major = interleaved x,y, int64 pair
+ *     arrays, the six int32/int8 triangulation arrays);
+ *   - calls are asynchronous on the given cudaStream_t (passed as void*);
+ *     no entry point synchronises the host or allocates device memory;
+ *     scratch comes from a caller-provided workspace sized by
+ *     bd_workspace_bytes();
+ *   - return value: 0 = launched OK, negative = CUDA launch error
+ *     (-(cudaError_t)); simulation outcomes (singularity, non-convergence,
+ *     rollback budget) are reported asynchronously in bd_stats_t.status.
+ */
+#ifndef BD_B200_H
+#define BD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (bd_stats_t.status), mapped to the reference exceptions
+ * core.py:18-45 by the Python layer */
+#define BD_OK 0
+#define BD_ERR_SINGULAR 1     /* SingularityError: zero separation (forces.py:55-58, :167-170) */
+#define BD_ERR_NONCONV 2      /* NonConvergenceError (dynamics.py:131, :247; triangulation.py:329) */
+#define BD_ERR_STEPFAIL 4     /* StepFailure: non-finite force / rollback budget (dynamics.py:84-86, :254-258) */
+#define BD_ERR_FLIP 5         /* BrownsimError: unflippable edge (triangulation.py:261-280) */
+#define BD_ERR_CAPACITY 6     /* a device buffer (Verlet pairs) is too small: host grows it and retries */
+
+/* force models of one step: long range (dynamics.py:194),
+ * short range over a Verlet list, or their sum F_LR + F_SR */
+#define BD_FORCE_LR 0
+#define BD_FORCE_SR 1
+#define BD_FORCE_LRSR 2
+
+/* all-pairs arithmetic: EXACT reproduces _kernels.long_range_kernel bit for
+ * bit; FAST uses fma + rsqrt/Newton (|dF|/|F| <= 1e-12) */
+#define BD_LR_EXACT 0
+#define BD_LR_FAST 1
+
+/* PeriodicTriangulation arrays, triangulation.py:129-139 */
+typedef struct bd_tri {
+    int64_t nv, ne, nt;
+    int32_t* tri_v;    /* (nt,3)   */
+    int8_t* tri_shift; /* (nt,3,2) */
+    int32_t* tri_edge; /* (nt,3)   */
+    int32_t* edge_v;   /* (ne,2)   */
+    int32_t* edge_tri; /* (ne,2)   */
+    int8_t* edge_opp;  /* (ne,2)   */
+} bd_tri_t;
+
+/* SimParams (core.py:161-204) + run constants */
+typedef struct bd_params {
+    int64_t n;
+    double L;
+    double sigma, dt, diffusion, cap, clamp, r_cut, skin, tol;
+    int64_t max_overlap_iters, max_rollbacks;
+    uint64_t seed, stream;
+    int64_t force_mode;   /* BD_FORCE_* */
+    int64_t lr_precision; /* BD_LR_* */
+    double mi_lo, mi_hi;  /* exact min-image breakpoints, filled by bd_prepare_params */
+    double r_list;        /* Verlet list radius max(r_cut, sigma) + skin */
+    int64_t ncx;          /* cells per axis of the Verlet grid (0 = all-pairs scan) */
+    int64_t pair_capacity;/* capacity of the Verlet pair buffers */
+} bd_params_t;
+
+/* StepStats (dynamics.py:42-57) counters + error report */
+typedef struct bd_stats {
+    double dt_used;
+    int64_t overlap_iterations, flip_passes, inversion_repairs, rollbacks, n_overlapping;
+    int64_t status, err_i, err_k;
+    int64_t rebuilds; /* Verlet rebuilds during this step */
+    int64_t reserved[6];
+} bd_stats_t;
+
+/* device state of one simulation */
+typedef struct bd_state {
+    double *pos, *prev, *force, *alpha, *mu; /* (n,2) (n,2) (n,2) (n,) (n,) */
+    int64_t* force_err;                      /* (n,) err sentinels of the force kernels */
+    int32_t* image;                          /* (n,2) unwrapped box images (MSD) */
+    uint8_t* overlap_flags;                  /* (n,) last_overlap_flags */
+    bd_tri_t tri;                            /* maintained triangulation */
+    bd_tri_t tri_backup;                     /* rollback copy (triangulation.py:158-164) */
+    uint64_t* call;                          /* noise call counter (1 element) */
+    bd_stats_t* stats;                       /* device stats of the last step */
+    /* Verlet list (forces.py:102-156): pairs, snapshot, count */
+    int64_t* pair_a;
+    int64_t* pair_b;
+    double* vl_snap;
+    int64_t* vl_meta; /* [0]=n_pairs, [1]=valid, [2]=rebuilds total */
+    void* work;       /* scratch of bd_workspace_bytes() bytes */
+    int64_t work_bytes;
+} bd_state_t;
+
+/* fills p->mi_lo/mi_hi (and r_list/ncx) from p->L etc.; host-only helper */
+void bd_prepare_params(bd_params_t* p);
+
+/* scratch bytes needed for n particles / ne edges / nt triangles / pair capacity */
+int64_t bd_workspace_bytes(int64_t n, int64_t ne, int64_t nt, int64_t pair_capacity);
+
+/* ---- kernel boundary (replaces brownsim._kernels) -------------------- */
+
+/* long_range_kernel (_kernels.py:26-59): out[i] = sum_{k != i} mu_i alpha_k
+ * r_ik / r^3 for receivers i in [i_begin, i_end) over all n sources;
+ * err[i] = k+1 on a zero-separation pair (else 0). out/err index the full
+ * range (rows outside [i_begin, i_end) are untouched). */
+int bd_long_range_forces(const double* pos, const double* alpha, const double* mu, int64_t n,
+                         double L, int64_t i_begin, int64_t i_end, int precision, double* out,
+                         int64_t* err, void* work, void* stream);
+
+/* scratch bytes of bd_long_range_forces (packed sources) */
+int64_t bd_long_range_workspace_bytes(int64_t n);
+
+/* short_range_kernel (_kernels.py:62-91) over stored pairs, accumulated
+ * per particle in ascending pair order (bit-exact). */
+int bd_short_range_forces(const double* pos, const double* alpha, const double* mu, int64_t n,
+                          const int64_t* pair_a, const int64_t* pair_b, int64_t n_pairs, double L,
+                          double r_cut, double* out, int64_t* err, void* work, void* stream);
+
+/* overlap_pass_kernel (_kernels.py:94-125): disp (n,2), flags (n,), count (1) */
+int bd_overlap_pass(const double* pos, int64_t n, const int64_t* pair_a, const int64_t* pair_b,
+                    int64_t n_pairs, double L, double sigma, double resolve, double* disp,
+                    uint8_t* flags, int64_t* count, void* work, void* stream);
+
+/* max_sq_displacement (_kernels.py:128-138) -> out[0] */
+int bd_max_sq_displacement(const double* pos, const double* snap, int64_t n, double L, double* out,
+                           void* stream);
+
+/* build_cell_grid + cell_pairs (forces.py:81-99, _kernels.py:141-236):
+ * ordered Verlet pair list identical to the reference's; writes count[0]
+ * (pairs are written only when count <= capacity). */
+int bd_verlet_build(const double* pos, int64_t n, double L, double r_list, int64_t* pair_a,
+                    int64_t* pair_b, int64_t capacity, int64_t* count, void* work,
+                    int64_t work_bytes, void* stream);
+
+/* counter-based normals for pairs [0, n_pairs) of one call */
+int bd_normals(uint64_t seed, uint64_t stream_id, uint64_t call, uint64_t purpose, int64_t n_pairs,
+               double* out, void* stream);
+
+/* ---- simulation boundary (replaces LongRangeSimulation.step etc.) ---- */
+
+/* the force evaluation of one step on the pre-move positions
+ * (dynamics.py:194) for p->force_mode; writes s->force and s->force_err */
+int bd_force(const bd_state_t* s, const bd_params_t* p, void* stream);
+
+/* the rest of LongRangeSimulation.step after the force (dynamics.py:196-274):
+ * integrate, pass-through check, inversion repair, Delaunay restoration,
+ * overlap correction with the joint fixed point, rollback -- one persistent
+ * kernel; StepStats counters to *out (device) */
+int bd_maintain_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, void* stream);
+
+/* one LongRangeSimulation.step (dynamics.py:191-274) with the force model of
+ * p->force_mode: force, integrate, pass-through check, inversion repair,
+ * Delaunay restoration, overlap correction, rollback -- all on device. */
+int bd_step_tri(const bd_state_t* s, const bd_params_t* p, void* stream);
+
+/* `steps` consecutive steps, stats of step j written to stats_out[j]
+ * (device array); stops at the first error. */
+int bd_run_tri(const bd_state_t* s, const bd_params_t* p, int64_t steps, bd_stats_t* stats_out,
+               void* stream);
+
+/* one ShortRangeSimulation.step (dynamics.py:326-346) */
+int bd_step_verlet(const bd_state_t* s, const bd_params_t* p, bd_stats_t* stats_out, void* stream);
+
+/* restore_delaunay (triangulation.py:319-334) on the state's triangulation
+ * and positions; passes (or -1 on error) written to passes_out[0] (device) */
+int bd_tri_restore_delaunay(const bd_state_t* s, const bd_params_t* p, int64_t* passes_out,
+                            void* stream);
+
+/* clears the sticky error status of a state (after the host handled it) */
+int bd_clear_status(const bd_state_t* s, void* stream);
+
+/* geometric audit counters (triangulation.py:386-482): out[0] = triangles
+ * with area2 <= 0, out[1] = edges violating the in-circle test */
+int bd_tri_audit_geometry(const bd_state_t* s, const bd_params_t* p, int64_t* out, void* stream);
+
+/* library version / build info (host) */
+const char* bd_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BD_B200_H */

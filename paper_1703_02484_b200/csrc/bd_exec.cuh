@@ -1,0 +1,214 @@
+// bd_exec.cuh -- execution policies for the device-resident step drivers.
+//
+// A step driver (bd_step.cuh) is written ONCE as uniform control flow over
+// data-parallel phases:
+//
+//     for (i = x.tid(); i < n; i += x.nth()) body(i);   // a phase
+//     v = R.close(slot);                                 // barrier + reduced value
+//
+// and instantiated with
+//   ExecGrid  -- persistent cooperative kernel, barrier = grid.sync()
+//   ExecBlock -- one CTA, barrier = __syncthreads()      (small N)
+//   ExecHost  -- one host thread, barrier = no-op         (tests/hostemu only:
+//                runs the identical driver logic on the CPU so control flow
+//                can be checked without a GPU; never used by the product)
+// Every thread executes the same sequence of barriers; decisions are made
+// only on values read after a barrier, so all threads take the same branch.
+#pragma once
+
+#include "bd_common.cuh"
+
+#if defined(__CUDACC__)
+#include <cooperative_groups.h>
+#endif
+
+namespace bd {
+
+typedef unsigned long long u64;
+
+// control block at the head of the workspace
+struct Ctl {
+    u64 red[8];     // reduction ring (see Red)
+    u64 status;     // first error code (BD_ERR_*), 0 = ok
+    u64 err_i, err_k;
+    u64 scratch[5];
+    u64 bsum[4096]; // per-block partial sums (grid scans)
+};
+
+#if defined(__CUDACC__)
+
+BD_DEV u64 ld_volatile(const u64* p) { return *(const volatile u64*)p; }
+
+// warp-aggregated atomic add (most lanes contribute 0)
+BD_DEV void atomic_add_u64(u64* p, u64 v) {
+    if (v) atomicAdd(p, v);
+}
+
+template <int NW>
+BD_DEV int64_t block_reduce_sum(int64_t v, int64_t* sh) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    int64_t t = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];
+    return t;
+}
+
+// exclusive scan of one value per thread over the block; returns the block total
+BD_DEV int64_t block_excl_scan(int64_t v, int64_t& excl, int64_t* sh) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    __syncthreads();
+    if (lane == 31) sh[w] = inc;
+    __syncthreads();
+    int64_t before = 0, total = 0;
+    for (int k = 0; k < nw; ++k) {
+        if (k < w) before += sh[k];
+        total += sh[k];
+    }
+    excl = before + inc - v;
+    return total;
+}
+
+struct ExecGrid {
+    Ctl* ctl;
+    BD_DEV int64_t tid() const { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
+    BD_DEV int64_t nth() const { return (int64_t)gridDim.x * blockDim.x; }
+    BD_DEV bool leader() const { return blockIdx.x == 0 && threadIdx.x == 0; }
+    BD_DEV void sync() { cooperative_groups::this_grid().sync(); }
+    BD_DEV void add(u64* p, u64 v) { atomic_add_u64(p, v); }
+    BD_DEV void umax(u64* p, u64 v) { atomicMax(p, v); }
+    BD_DEV void umin(u64* p, u64 v) { atomicMin(p, v); }
+    BD_DEV u64 cas(u64* p, u64 cmp, u64 v) { return atomicCAS(p, cmp, v); }
+    BD_DEV int32_t fetch_add32(int32_t* p, int32_t v) { return atomicAdd(p, v); }
+    BD_DEV u64 ld(const u64* p) const { return ld_volatile(p); }
+
+    // in-place exclusive scan of a[0..n) (int32), a[n] = total; ends with a barrier
+    BD_DEV void exclusive_scan(int32_t* a, int64_t n) {
+        __shared__ int64_t sh[32];
+        const int64_t nb = gridDim.x, b = blockIdx.x;
+        const int64_t R = (n + nb - 1) / nb;
+        const int64_t lo = b * R < n ? b * R : n, hi = (b + 1) * R < n ? (b + 1) * R : n;
+        int64_t part = 0;
+        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) part += a[i];
+        part = block_reduce_sum<32>(part, sh);
+        if (threadIdx.x == 0) ctl->bsum[b] = (u64)part;
+        sync();
+        int64_t pre = 0;
+        for (int64_t j = threadIdx.x; j < b; j += blockDim.x) pre += (int64_t)ld_volatile(&ctl->bsum[j]);
+        pre = block_reduce_sum<32>(pre, sh);
+        int64_t carry = pre;
+        for (int64_t base = lo; base < hi; base += blockDim.x) {
+            int64_t i = base + threadIdx.x;
+            int64_t v = i < hi ? a[i] : 0, ex;
+            int64_t tot = block_excl_scan(v, ex, sh);
+            if (i < hi) a[i] = (int32_t)(carry + ex);
+            carry += tot;
+            __syncthreads();
+        }
+        if (b == nb - 1 && threadIdx.x == 0) a[n] = (int32_t)carry;
+        sync();
+    }
+};
+
+struct ExecBlock {
+    Ctl* ctl;
+    BD_DEV int64_t tid() const { return threadIdx.x; }
+    BD_DEV int64_t nth() const { return blockDim.x; }
+    BD_DEV bool leader() const { return threadIdx.x == 0; }
+    BD_DEV void sync() {
+        __threadfence_block();
+        __syncthreads();
+    }
+    BD_DEV void add(u64* p, u64 v) { atomic_add_u64(p, v); }
+    BD_DEV void umax(u64* p, u64 v) { atomicMax(p, v); }
+    BD_DEV void umin(u64* p, u64 v) { atomicMin(p, v); }
+    BD_DEV u64 cas(u64* p, u64 cmp, u64 v) { return atomicCAS(p, cmp, v); }
+    BD_DEV int32_t fetch_add32(int32_t* p, int32_t v) { return atomicAdd(p, v); }
+    BD_DEV u64 ld(const u64* p) const { return ld_volatile(p); }
+
+    BD_DEV void exclusive_scan(int32_t* a, int64_t n) {
+        __shared__ int64_t sh[32];
+        int64_t carry = 0;
+        for (int64_t base = 0; base < n; base += blockDim.x) {
+            int64_t i = base + threadIdx.x;
+            int64_t v = i < n ? a[i] : 0, ex;
+            int64_t tot = block_excl_scan(v, ex, sh);
+            if (i < n) a[i] = (int32_t)(carry + ex);
+            carry += tot;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) a[n] = (int32_t)carry;
+        sync();
+    }
+};
+
+#endif  // __CUDACC__
+
+// host emulation (tests only): one "thread" covering every element in order
+struct ExecHost {
+    Ctl* ctl;
+    int64_t tid() const { return 0; }
+    int64_t nth() const { return 1; }
+    bool leader() const { return true; }
+    void sync() {}
+    void add(u64* p, u64 v) { *p += v; }
+    void umax(u64* p, u64 v) {
+        if (v > *p) *p = v;
+    }
+    void umin(u64* p, u64 v) {
+        if (v < *p) *p = v;
+    }
+    u64 cas(u64* p, u64 cmp, u64 v) {
+        u64 old = *p;
+        if (old == cmp) *p = v;
+        return old;
+    }
+    int32_t fetch_add32(int32_t* p, int32_t v) {
+        int32_t o = *p;
+        *p += v;
+        return o;
+    }
+    u64 ld(const u64* p) const { return *p; }
+    void exclusive_scan(int32_t* a, int64_t n) {
+        int64_t c = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            int64_t v = a[i];
+            a[i] = (int32_t)c;
+            c += v;
+        }
+        a[n] = (int32_t)c;
+    }
+};
+
+// Reduction ring: reduction k accumulates into red[k & 7]; whoever opens
+// reduction k zeroes red[(k+1) & 7] for the next one.  That slot was last
+// read right after the barrier of reduction k-7, so no thread can still be
+// reading it, and the barrier closing reduction k publishes the zero before
+// reduction k+1 accumulates.  All threads open/close in lockstep.
+template <class X>
+struct Red {
+    X& x;
+    unsigned k;
+    BD_HD explicit Red(X& x_) : x(x_), k(0) {}
+    BD_HD u64* open() {
+        if (x.leader()) x.ctl->red[(k + 1) & 7] = 0;
+        return &x.ctl->red[k & 7];
+    }
+    BD_HD u64 close(u64* s) {
+        x.sync();
+        u64 v = x.ld(s);
+        ++k;
+        return v;
+    }
+};
+
+}  // namespace bd

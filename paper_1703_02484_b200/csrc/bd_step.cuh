@@ -1,0 +1,650 @@
+// bd_step.cuh -- device-resident step driver (one source, three policies).
+//
+// Restates LongRangeSimulation.step (dynamics.py:191-274) and its callees
+// (integrate dynamics.py:73-94, correct_overlaps :97-133, the triangulation
+// maintenance triangulation.py:166-363) as uniform phases over particles,
+// edges and triangles, separated by barriers (see bd_exec.cuh).
+//
+// Bit-exactness: every floating-point expression follows the reference's
+// evaluation order; per-particle sums that the reference accumulates in
+// ascending pair order are gathered per particle over an incidence list
+// sorted by pair index, so the GPU result is bit-identical to the reference
+// (and to oracle/bd_oracle.c) on the same inputs and noise.
+#pragma once
+
+#include "bd_exec.cuh"
+
+namespace bd {
+
+enum : uint8_t { ES_NONE = 0, ES_UND = 1, ES_SEL = 2, ES_REM = 3 };
+
+// workspace carve-up (device pointers)
+struct Ws {
+    Ctl* ctl;
+    double* contrib;   // (ne,2) per-edge bounce displacement of the current sweep
+    uint8_t* estat;    // (ne) flag / selection status
+    uint8_t* eovl;     // (ne) edge overlapping this sweep
+    uint8_t* tinv;     // (nt) triangle inverted
+    int8_t* cross8;    // (n,2) crossings mod 256 (all apply_crossings needs)
+    int32_t* image_bk; // (n,2)
+    int32_t* inc_off;  // (n+1) CSR offsets of incident edges
+    int32_t* inc_cur;  // (n) fill cursors
+    int32_t* inc;      // (2 ne) incident edges, ascending per vertex
+    double* src4;      // (n,4) packed {x, y, alpha, 0} sources of the all-pairs kernel
+};
+
+BD_HD int64_t align_up(int64_t x) { return (x + 255) & ~(int64_t)255; }
+
+// layout of bd_workspace_bytes(); offsets relative to the workspace base
+struct WsLayout {
+    int64_t ctl, contrib, estat, eovl, tinv, cross8, image_bk, inc_off, inc_cur, inc, src4, total;
+};
+
+BD_HD WsLayout ws_layout(int64_t n, int64_t ne, int64_t nt) {
+    WsLayout l;
+    int64_t o = 0;
+    l.ctl = o; o = align_up(o + (int64_t)sizeof(Ctl));
+    l.contrib = o; o = align_up(o + 16 * ne);
+    l.estat = o; o = align_up(o + ne);
+    l.eovl = o; o = align_up(o + ne);
+    l.tinv = o; o = align_up(o + nt);
+    l.cross8 = o; o = align_up(o + 2 * n);
+    l.image_bk = o; o = align_up(o + 8 * n);
+    l.inc_off = o; o = align_up(o + 4 * (n + 1));
+    l.inc_cur = o; o = align_up(o + 4 * n);
+    l.inc = o; o = align_up(o + 8 * ne);
+    l.src4 = o; o = align_up(o + 32 * n);
+    l.total = o;
+    return l;
+}
+
+BD_HD Ws ws_carve(void* base, int64_t n, int64_t ne, int64_t nt) {
+    WsLayout l = ws_layout(n, ne, nt);
+    char* b = (char*)base;
+    Ws w;
+    w.ctl = (Ctl*)(b + l.ctl);
+    w.contrib = (double*)(b + l.contrib);
+    w.estat = (uint8_t*)(b + l.estat);
+    w.eovl = (uint8_t*)(b + l.eovl);
+    w.tinv = (uint8_t*)(b + l.tinv);
+    w.cross8 = (int8_t*)(b + l.cross8);
+    w.image_bk = (int32_t*)(b + l.image_bk);
+    w.inc_off = (int32_t*)(b + l.inc_off);
+    w.inc_cur = (int32_t*)(b + l.inc_cur);
+    w.inc = (int32_t*)(b + l.inc);
+    w.src4 = (double*)(b + l.src4);
+    return w;
+}
+
+struct Ctx {
+    bd_params_t p;
+    bd_state_t s;
+    Ws w;
+    uint64_t call;
+};
+
+template <class X>
+BD_HD void set_error(X& x, Ctx& c, u64 code, int64_t i, int64_t k) {
+    if (x.cas(&c.w.ctl->status, 0, code) == 0) {
+        c.w.ctl->err_i = (u64)i;
+        c.w.ctl->err_k = (u64)k;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// small per-element helpers
+
+BD_HD double tri_coord(const bd_tri_t& T, const double* pos, double L, int64_t t, int k, int c) {
+    return pos[2 * (int64_t)T.tri_v[3 * t + k] + c] + (double)T.tri_shift[6 * t + 2 * k + c] * L;
+}
+
+BD_HD void tri_xy(const bd_tri_t& T, const double* pos, double L, int64_t t, V2 xy[3]) {
+    for (int k = 0; k < 3; ++k) {
+        xy[k].x = tri_coord(T, pos, L, t, k, 0);
+        xy[k].y = tri_coord(T, pos, L, t, k, 1);
+    }
+}
+
+// edge_quads, triangulation.py:193-222
+BD_HD void edge_quad(const bd_tri_t& T, const double* pos, double L, int64_t e, V2 q[4]) {
+    const int64_t tl = T.edge_tri[2 * e], tr = T.edge_tri[2 * e + 1];
+    const int ol = T.edge_opp[2 * e], orr = T.edge_opp[2 * e + 1];
+    const int a_sl = (ol + 1) % 3, b_sl = (ol + 2) % 3, a_sr = (orr + 2) % 3;
+    const int8_t* sl = T.tri_shift + 6 * tl;
+    const int8_t* sr = T.tri_shift + 6 * tr;
+    q[0] = emb(pos, T.tri_v[3 * tl + a_sl], (double)sl[2 * a_sl], (double)sl[2 * a_sl + 1], L);
+    q[1] = emb(pos, T.tri_v[3 * tl + b_sl], (double)sl[2 * b_sl], (double)sl[2 * b_sl + 1], L);
+    q[2] = emb(pos, T.tri_v[3 * tl + ol], (double)sl[2 * ol], (double)sl[2 * ol + 1], L);
+    const double dlx = (double)sl[2 * a_sl] - (double)sr[2 * a_sr];
+    const double dly = (double)sl[2 * a_sl + 1] - (double)sr[2 * a_sr + 1];
+    q[3] = emb(pos, T.tri_v[3 * tr + orr], (double)sr[2 * orr] + dlx, (double)sr[2 * orr + 1] + dly, L);
+}
+
+// one side of _crossed_edges (triangulation.py:365-382): did the path of the
+// vertex in slot k of triangle t cross the opposite edge?
+BD_HD bool crossed_side(const bd_tri_t& T, const double* pos, const double* prv, const bd_params_t& p,
+                        int64_t t, int k) {
+    V2 xy[3];
+    tri_xy(T, pos, p.L, t, xy);
+    const int64_t w = T.tri_v[3 * t + k];
+    const double sx = mi_exact(pos[2 * w] - prv[2 * w], p), sy = mi_exact(pos[2 * w + 1] - prv[2 * w + 1], p);
+    V2 ps;
+    ps.x = xy[k].x - sx;
+    ps.y = xy[k].y - sy;
+    return seg_intersect(ps, xy[k], xy[(k + 1) % 3], xy[(k + 2) % 3]);
+}
+
+// flip_edge + _relink, triangulation.py:254-302 (conflict-free flips may run concurrently)
+BD_HD void relink(bd_tri_t& T, int64_t edge, int32_t old_tri, int32_t new_tri, int8_t opp) {
+    const int side = T.edge_tri[2 * edge] == old_tri ? 0 : 1;
+    T.edge_tri[2 * edge + side] = new_tri;
+    T.edge_opp[2 * edge + side] = opp;
+}
+
+BD_HD int flip_edge(bd_tri_t& T, int64_t e) {
+    const int32_t tl = T.edge_tri[2 * e], tr = T.edge_tri[2 * e + 1];
+    if (tl == tr) return BD_ERR_FLIP;
+    const int ol = T.edge_opp[2 * e], orr = T.edge_opp[2 * e + 1];
+    const int a_sl = (ol + 1) % 3, b_sl = (ol + 2) % 3, b_sr = (orr + 1) % 3, a_sr = (orr + 2) % 3;
+    const int32_t va = T.tri_v[3 * tl + a_sl], vb = T.tri_v[3 * tl + b_sl];
+    const int32_t vc = T.tri_v[3 * tl + ol], vd = T.tri_v[3 * tr + orr];
+    int32_t sa[2], sb[2], sc[2], sd[2];
+    for (int c = 0; c < 2; ++c) {
+        sa[c] = T.tri_shift[6 * tl + 2 * a_sl + c];
+        sb[c] = T.tri_shift[6 * tl + 2 * b_sl + c];
+        sc[c] = T.tri_shift[6 * tl + 2 * ol + c];
+        sd[c] = (int32_t)T.tri_shift[6 * tr + 2 * orr + c] + (sa[c] - (int32_t)T.tri_shift[6 * tr + 2 * a_sr + c]);
+    }
+    const int32_t e_bc = T.tri_edge[3 * tl + a_sl], e_ca = T.tri_edge[3 * tl + b_sl];
+    const int32_t e_ad = T.tri_edge[3 * tr + b_sr], e_db = T.tri_edge[3 * tr + a_sr];
+    const int64_t ids[5] = {e, e_bc, e_ca, e_ad, e_db};
+    for (int i = 0; i < 5; ++i)
+        for (int j = i + 1; j < 5; ++j)
+            if (ids[i] == ids[j]) return BD_ERR_FLIP;
+    T.tri_v[3 * tl] = vc; T.tri_v[3 * tl + 1] = va; T.tri_v[3 * tl + 2] = vd;
+    T.tri_v[3 * tr] = vd; T.tri_v[3 * tr + 1] = vb; T.tri_v[3 * tr + 2] = vc;
+    for (int c = 0; c < 2; ++c) {
+        T.tri_shift[6 * tl + c] = 0;
+        T.tri_shift[6 * tl + 2 + c] = (int8_t)(sa[c] - sc[c]);
+        T.tri_shift[6 * tl + 4 + c] = (int8_t)(sd[c] - sc[c]);
+        T.tri_shift[6 * tr + c] = 0;
+        T.tri_shift[6 * tr + 2 + c] = (int8_t)(sb[c] - sd[c]);
+        T.tri_shift[6 * tr + 4 + c] = (int8_t)(sc[c] - sd[c]);
+    }
+    T.tri_edge[3 * tl] = e_ad; T.tri_edge[3 * tl + 1] = (int32_t)e; T.tri_edge[3 * tl + 2] = e_ca;
+    T.tri_edge[3 * tr] = e_bc; T.tri_edge[3 * tr + 1] = (int32_t)e; T.tri_edge[3 * tr + 2] = e_db;
+    T.edge_v[2 * e] = vc; T.edge_v[2 * e + 1] = vd;
+    T.edge_tri[2 * e] = tr; T.edge_tri[2 * e + 1] = tl;
+    T.edge_opp[2 * e] = 1; T.edge_opp[2 * e + 1] = 1;
+    relink(T, e_ca, tl, tl, 2);
+    relink(T, e_ad, tr, tl, 0);
+    relink(T, e_bc, tl, tr, 0);
+    relink(T, e_db, tr, tr, 2);
+    return BD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// phases
+
+// copy the six triangulation arrays a -> b (save_state / restore_state)
+template <class X>
+BD_HD void ph_tri_copy(X& x, const bd_tri_t& a, bd_tri_t& b) {
+    for (int64_t t = x.tid(); t < a.nt; t += x.nth()) {
+        for (int k = 0; k < 3; ++k) {
+            b.tri_v[3 * t + k] = a.tri_v[3 * t + k];
+            b.tri_edge[3 * t + k] = a.tri_edge[3 * t + k];
+        }
+        for (int k = 0; k < 6; ++k) b.tri_shift[6 * t + k] = a.tri_shift[6 * t + k];
+    }
+    for (int64_t e = x.tid(); e < a.ne; e += x.nth()) {
+        b.edge_v[2 * e] = a.edge_v[2 * e];
+        b.edge_v[2 * e + 1] = a.edge_v[2 * e + 1];
+        b.edge_tri[2 * e] = a.edge_tri[2 * e];
+        b.edge_tri[2 * e + 1] = a.edge_tri[2 * e + 1];
+        b.edge_opp[2 * e] = a.edge_opp[2 * e];
+        b.edge_opp[2 * e + 1] = a.edge_opp[2 * e + 1];
+    }
+}
+
+// integrate (dynamics.py:73-94) fused with the crossing bookkeeping; returns #particles that crossed
+template <class X>
+BD_HD u64 ph_integrate(X& x, Red<X>& R, Ctx& c, double dt) {
+    u64* r = R.open();
+    const double L = c.p.L, scale = sqrt(c.p.diffusion * dt), clamp = c.p.clamp;
+    double* pos = c.s.pos;
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
+        double z0, z1;
+        normal_pair(c.p.seed, c.p.stream, c.call, (uint64_t)i, 0, z0, z1);
+        const double z[2] = {clampd(z0, clamp), clampd(z1, clamp)};
+        int crossed = 0;
+        for (int k = 0; k < 2; ++k) {
+            const double p0 = pos[2 * i + k];
+            c.s.prev[2 * i + k] = p0;
+            const double nw = p0 + c.s.force[2 * i + k] * dt + z[k] * scale;
+            const double w = wrap1(nw, L);
+            const long long ci = (long long)rint((nw - w) / L);
+            pos[2 * i + k] = w;
+            c.w.cross8[2 * i + k] = (int8_t)ci;
+            if (c.s.image) c.s.image[2 * i + k] += (int32_t)ci;
+            crossed |= ci != 0;
+        }
+        x.add(r, (u64)crossed);
+    }
+    return R.close(r);
+}
+
+// apply_crossings (triangulation.py:166-177), only called when some particle crossed
+template <class X>
+BD_HD void ph_apply_crossings(X& x, Ctx& c) {
+    bd_tri_t& T = c.s.tri;
+    for (int64_t t = x.tid(); t < T.nt; t += x.nth()) {
+        int32_t ts[3][2];
+        for (int k = 0; k < 3; ++k)
+            for (int q = 0; q < 2; ++q)
+                ts[k][q] = (int32_t)T.tri_shift[6 * t + 2 * k + q] + (int32_t)c.w.cross8[2 * (int64_t)T.tri_v[3 * t + k] + q];
+        for (int k = 0; k < 3; ++k)
+            for (int q = 0; q < 2; ++q) T.tri_shift[6 * t + 2 * k + q] = (int8_t)(ts[k][q] - ts[0][q]);
+    }
+    x.sync();
+}
+
+// edge_inversion_present (triangulation.py:240-250)
+template <class X>
+BD_HD bool ph_edge_inversion(X& x, Red<X>& R, Ctx& c) {
+    u64* r = R.open();
+    const bd_tri_t& T = c.s.tri;
+    const double* prev = c.s.prev;
+    const double* cur = c.s.pos;
+    for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+        const int64_t a = T.edge_v[2 * e], b = T.edge_v[2 * e + 1];
+        const double d0x = mi_exact(prev[2 * b] - prev[2 * a], c.p), d0y = mi_exact(prev[2 * b + 1] - prev[2 * a + 1], c.p);
+        const double d1x = mi_exact(cur[2 * b] - cur[2 * a], c.p), d1y = mi_exact(cur[2 * b + 1] - cur[2 * a + 1], c.p);
+        x.add(r, (u64)(d0x * d1x + d0y * d1y < 0.0));
+    }
+    return R.close(r) != 0;
+}
+
+// signed_area2 <= 0 per triangle; returns #inverted
+template <class X>
+BD_HD u64 ph_inverted_tris(X& x, Red<X>& R, Ctx& c) {
+    u64* r = R.open();
+    const bd_tri_t& T = c.s.tri;
+    for (int64_t t = x.tid(); t < T.nt; t += x.nth()) {
+        V2 xy[3];
+        tri_xy(T, c.s.pos, c.p.L, t, xy);
+        const double e1x = xy[1].x - xy[0].x, e1y = xy[1].y - xy[0].y;
+        const double e2x = xy[2].x - xy[0].x, e2y = xy[2].y - xy[0].y;
+        const bool inv = e1x * e2y - e1y * e2x <= 0.0;
+        c.w.tinv[t] = (uint8_t)inv;
+        x.add(r, (u64)inv);
+    }
+    return R.close(r);
+}
+
+// lexicographically-first maximal independent set of the flagged edges
+// (== the reference's greedy ascending scan, triangulation.py:304-315),
+// then the flips of the selected edges.  Returns #flips.
+template <class X>
+BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c) {
+    bd_tri_t& T = c.s.tri;
+    uint8_t* st = c.w.estat;
+    u64 nsel_total = 0;
+    for (;;) {
+        u64* rs = R.open();
+        for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+            if (st[e] != ES_UND) continue;
+            bool win = true;
+            for (int side = 0; side < 2 && win; ++side) {
+                const int64_t t = T.edge_tri[2 * e + side];
+                for (int k = 0; k < 3; ++k) {
+                    const int64_t f = T.tri_edge[3 * t + k];
+                    if (f < e) {
+                        const uint8_t sf = st[f];
+                        if (sf == ES_UND || sf == ES_SEL) {
+                            win = false;
+                            break;
+                        }
+                    }
+                }
+            }
+            if (win) st[e] = ES_SEL;
+            x.add(rs, (u64)win);
+        }
+        nsel_total += R.close(rs);
+        u64* ru = R.open();
+        for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+            if (st[e] != ES_UND) continue;
+            bool blocked = false;
+            for (int side = 0; side < 2 && !blocked; ++side) {
+                const int64_t t = T.edge_tri[2 * e + side];
+                for (int k = 0; k < 3; ++k) {
+                    const int64_t f = T.tri_edge[3 * t + k];
+                    if (f != e && st[f] == ES_SEL) {
+                        blocked = true;
+                        break;
+                    }
+                }
+            }
+            if (blocked) st[e] = ES_REM;
+            x.add(ru, (u64)!blocked);
+        }
+        if (R.close(ru) == 0) break;
+    }
+    if (nsel_total == 0) return 0;
+    for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+        if (st[e] != ES_SEL) continue;
+        const int rc = flip_edge(T, e);
+        if (rc) set_error(x, c, (u64)rc, e, 0);
+    }
+    x.sync();
+    return nsel_total;
+}
+
+// restore_delaunay (triangulation.py:319-334); returns passes, or -1 on error
+template <class X>
+BD_HD int64_t restore_delaunay(X& x, Red<X>& R, Ctx& c, int64_t max_passes) {
+    bd_tri_t& T = c.s.tri;
+    int64_t passes = 0;
+    for (;;) {
+        u64* r = R.open();
+        for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+            V2 q[4];
+            edge_quad(T, c.s.pos, c.p.L, e, q);
+            const bool f = incircle(q[0], q[1], q[2], q[3], c.p.tol);
+            c.w.estat[e] = f ? ES_UND : ES_NONE;
+            x.add(r, (u64)f);
+        }
+        if (R.close(r) == 0) return passes;
+        passes++;
+        if (passes > max_passes) {
+            set_error(x, c, BD_ERR_NONCONV, passes, 0);
+            x.sync();
+            return -1;
+        }
+        ph_select_and_flip(x, R, c);
+        if (x.ld(&c.w.ctl->status)) return -1;
+    }
+}
+
+// repair_inversions (triangulation.py:336-363) with prev = positions_prev.
+// returns 0 ok, 1 needs rollback, -1 error; adds flips to *flips
+template <class X>
+BD_HD int repair_inversions(X& x, Red<X>& R, Ctx& c, int64_t max_passes, int64_t* flips) {
+    bd_tri_t& T = c.s.tri;
+    for (int64_t pass = 0; pass < max_passes; ++pass) {
+        if (ph_inverted_tris(x, R, c) == 0) return 0;
+        for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+            V2 q[4];
+            edge_quad(T, c.s.pos, c.p.L, e, q);
+            bool f = point_in_tri(q[3], q[0], q[1], q[2]) | point_in_tri(q[2], q[0], q[1], q[3]);
+            for (int side = 0; side < 2 && !f; ++side) {
+                const int64_t t = T.edge_tri[2 * e + side];
+                if (c.w.tinv[t]) f = crossed_side(T, c.s.pos, c.s.prev, c.p, t, T.edge_opp[2 * e + side]);
+            }
+            c.w.estat[e] = f ? ES_UND : ES_NONE;
+        }
+        x.sync();
+        const u64 chosen = ph_select_and_flip(x, R, c);
+        if (x.ld(&c.w.ctl->status)) return -1;
+        if (chosen == 0) return 1;
+        *flips += (int64_t)chosen;
+    }
+    return ph_inverted_tris(x, R, c) != 0 ? 1 : 0;
+}
+
+// edge_inversion_present + repair_inversions + restore_delaunay
+// (dynamics.py:206-214 and :236-242): 0 ok, 1 rollback, -1 error
+template <class X>
+BD_HD int maintain(X& x, Red<X>& R, Ctx& c, int64_t* repairs, int64_t* flip_passes) {
+    if (ph_edge_inversion(x, R, c)) return 1;
+    const int rr = repair_inversions(x, R, c, 10, repairs);
+    if (rr) return rr;
+    const int64_t p = restore_delaunay(x, R, c, 1000);
+    if (p < 0) return -1;
+    *flip_passes += p;
+    return 0;
+}
+
+// vertex -> incident edges, ascending edge id (fixes the reference's
+// ascending-pair accumulation order of overlap_pass_kernel)
+template <class X>
+BD_HD void build_incidence(X& x, Ctx& c) {
+    const bd_tri_t& T = c.s.tri;
+    const int64_t n = c.p.n;
+    int32_t* off = c.w.inc_off;
+    for (int64_t i = x.tid(); i < n; i += x.nth()) {
+        off[i] = 0;
+        c.w.inc_cur[i] = 0;
+    }
+    x.sync();
+    for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+        x.fetch_add32(&off[T.edge_v[2 * e]], 1);
+        x.fetch_add32(&off[T.edge_v[2 * e + 1]], 1);
+    }
+    x.sync();
+    x.exclusive_scan(off, n);
+    for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+        const int64_t a = T.edge_v[2 * e], b = T.edge_v[2 * e + 1];
+        c.w.inc[off[a] + x.fetch_add32(&c.w.inc_cur[a], 1)] = (int32_t)e;
+        c.w.inc[off[b] + x.fetch_add32(&c.w.inc_cur[b], 1)] = (int32_t)e;
+    }
+    x.sync();
+    for (int64_t i = x.tid(); i < n; i += x.nth()) {
+        int32_t* L = c.w.inc + off[i];
+        const int32_t m = off[i + 1] - off[i];
+        for (int32_t j = 1; j < m; ++j) {
+            const int32_t v = L[j];
+            int32_t k = j - 1;
+            while (k >= 0 && L[k] > v) {
+                L[k + 1] = L[k];
+                --k;
+            }
+            L[k + 1] = v;
+        }
+    }
+    x.sync();
+}
+
+// correct_overlaps (dynamics.py:97-133) over the triangulation edges; returns
+// sweeps, or -1 on non-convergence
+template <class X>
+BD_HD int64_t correct_overlaps_tri(X& x, Red<X>& R, Ctx& c) {
+    const bd_tri_t& T = c.s.tri;
+    const double L = c.p.L, sigma = c.p.sigma, thresh = sigma * (1.0 - 1e-9), cap = c.p.cap;
+    double* pos = c.s.pos;
+    int64_t iterations = 0;
+    for (int64_t it = 0; it < c.p.max_overlap_iters; ++it) {
+        u64* r = R.open();
+        for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+            const int64_t a = T.edge_v[2 * e], b = T.edge_v[2 * e + 1];
+            const double dx = mi_exact(pos[2 * b] - pos[2 * a], c.p), dy = mi_exact(pos[2 * b + 1] - pos[2 * a + 1], c.p);
+            const double rr = sqrt(dx * dx + dy * dy);
+            const bool ov = !(rr >= thresh || rr == 0.0);
+            if (ov) {
+                const double delta = sigma - rr;
+                const double ux = dx / rr, uy = dy / rr;
+                c.w.contrib[2 * e] = delta * ux;
+                c.w.contrib[2 * e + 1] = delta * uy;
+            }
+            c.w.eovl[e] = (uint8_t)ov;
+            x.add(r, (u64)ov);
+        }
+        if (R.close(r) == 0) return iterations;
+        iterations++;
+        u64* rc = R.open();
+        for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
+            double dx = 0.0, dy = 0.0;
+            bool hit = false;
+            const int32_t j0 = c.w.inc_off[i], j1 = c.w.inc_off[i + 1];
+            for (int32_t j = j0; j < j1; ++j) {
+                const int64_t e = c.w.inc[j];
+                if (!c.w.eovl[e]) continue;
+                hit = true;
+                const double cx = c.w.contrib[2 * e], cy = c.w.contrib[2 * e + 1];
+                if (T.edge_v[2 * e] == i) {
+                    dx -= cx;
+                    dy -= cy;
+                } else {
+                    dx += cx;
+                    dy += cy;
+                }
+            }
+            int crossed = 0;
+            if (hit) {
+                c.s.overlap_flags[i] = 1;
+                const double norm = sqrt(dx * dx + dy * dy);
+                double factor = 1.0;
+                if (norm > cap) factor = cap / norm;
+                const double d[2] = {dx, dy};
+                for (int k = 0; k < 2; ++k) {
+                    const double nw = pos[2 * i + k] + d[k] * factor;
+                    const double w = wrap1(nw, L);
+                    const long long ci = (long long)rint((nw - w) / L);
+                    pos[2 * i + k] = w;
+                    c.w.cross8[2 * i + k] = (int8_t)ci;
+                    if (c.s.image) c.s.image[2 * i + k] += (int32_t)ci;
+                    crossed |= ci != 0;
+                }
+            } else {
+                c.w.cross8[2 * i] = 0;
+                c.w.cross8[2 * i + 1] = 0;
+            }
+            x.add(rc, (u64)crossed);
+        }
+        if (R.close(rc)) ph_apply_crossings(x, c);
+    }
+    set_error(x, c, BD_ERR_NONCONV, 0, 0);
+    x.sync();
+    return -1;
+}
+
+// LongRangeSimulation.step after the force evaluation (dynamics.py:196-274).
+// The forces of this step are already in s.force (computed by the all-pairs
+// kernel / Verlet force on the pre-move positions).
+template <class X>
+BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
+    Red<X> R(x);
+    if (x.leader())
+        for (int k = 0; k < 8; ++k) c.w.ctl->red[k] = 0;
+    x.sync();
+    if (x.ld(&c.w.ctl->status)) {  // an earlier step failed: this one does not run
+        if (x.leader()) out->status = -1;
+        return;
+    }
+    // singularity sentinels of the force kernels (forces.py:54-58: first i, k = err[i]-1)
+    {
+        u64* r = R.open();
+        if (x.leader()) c.w.ctl->scratch[1] = ~0ull;
+        x.sync();
+        for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
+            const bool bad = c.s.force_err[i] != 0;
+            if (bad) x.umin(&c.w.ctl->scratch[1], (u64)i);
+            x.add(r, (u64)bad);
+        }
+        if (R.close(r)) {
+            if (x.leader()) {
+                const int64_t i = (int64_t)c.w.ctl->scratch[1];
+                c.w.ctl->status = BD_ERR_SINGULAR;
+                c.w.ctl->err_i = (u64)i;
+                c.w.ctl->err_k = (u64)(c.s.force_err[i] - 1);
+                out->status = BD_ERR_SINGULAR;
+                out->err_i = i;
+                out->err_k = c.s.force_err[i] - 1;
+            }
+            return;
+        }
+    }
+    // finite-force check (integrate, dynamics.py:84-86)
+    {
+        u64* r = R.open();
+        if (x.leader()) c.w.ctl->scratch[0] = ~0ull;
+        x.sync();
+        for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
+            const bool bad = !(isfinite(c.s.force[2 * i]) && isfinite(c.s.force[2 * i + 1]));
+            if (bad) x.umin(&c.w.ctl->scratch[0], (u64)i);
+            x.add(r, (u64)bad);
+        }
+        if (R.close(r)) {
+            if (x.leader()) {
+                c.w.ctl->status = BD_ERR_STEPFAIL;
+                c.w.ctl->err_i = c.w.ctl->scratch[0];
+                out->status = BD_ERR_STEPFAIL;
+                out->err_i = (int64_t)c.w.ctl->scratch[0];
+            }
+            return;
+        }
+    }
+    // save_state (triangulation.py:158-160) + image counters
+    ph_tri_copy(x, c.s.tri, c.s.tri_backup);
+    if (c.s.image)
+        for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.w.image_bk[i] = c.s.image[i];
+    x.sync();
+
+    double dt_try = c.p.dt;
+    int64_t rollbacks = 0, iters = 0, repairs = 0, flip_passes = 0;
+    bool failed = false;
+    for (;;) {
+        const u64 nc = ph_integrate(x, R, c, dt_try);
+        c.call++;
+        if (nc) ph_apply_crossings(x, c);
+        repairs = 0;
+        flip_passes = 0;
+        int m = maintain(x, R, c, &repairs, &flip_passes);
+        if (m < 0) break;
+        failed = m == 1;
+        if (!failed) {
+            iters = 0;
+            for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) c.s.overlap_flags[i] = 0;
+            int64_t outer;
+            for (outer = 0; outer < c.p.max_overlap_iters; ++outer) {
+                build_incidence(x, c);
+                const int64_t ri = correct_overlaps_tri(x, R, c);
+                if (ri < 0) break;
+                iters += ri;
+                if (ri == 0) break;
+                m = maintain(x, R, c, &repairs, &flip_passes);
+                if (m < 0) break;
+                failed = m == 1;
+                if (failed) break;
+            }
+            if (x.ld(&c.w.ctl->status)) break;
+            if (outer == c.p.max_overlap_iters) {
+                set_error(x, c, BD_ERR_NONCONV, 0, 0);
+                x.sync();
+                break;
+            }
+        }
+        if (!failed) break;
+        rollbacks++;
+        if (rollbacks > c.p.max_rollbacks) {
+            set_error(x, c, BD_ERR_STEPFAIL, rollbacks, 0);
+            x.sync();
+            break;
+        }
+        // restore_prev + restore_state, dt halving (dynamics.py:259-261)
+        for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.s.pos[i] = c.s.prev[i];
+        if (c.s.image)
+            for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.s.image[i] = c.w.image_bk[i];
+        ph_tri_copy(x, c.s.tri_backup, c.s.tri);
+        x.sync();
+        dt_try *= 0.5;
+    }
+    // n_overlapping
+    u64* r = R.open();
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) x.add(r, (u64)c.s.overlap_flags[i]);
+    const u64 nov = R.close(r);
+    if (x.leader()) {
+        out->dt_used = dt_try;
+        out->overlap_iterations = iters;
+        out->flip_passes = flip_passes;
+        out->inversion_repairs = repairs;
+        out->rollbacks = rollbacks;
+        out->n_overlapping = (int64_t)nov;
+        out->status = (int64_t)c.w.ctl->status;
+        out->err_i = (int64_t)c.w.ctl->err_i;
+        out->err_k = (int64_t)c.w.ctl->err_k;
+        *c.s.call = c.call;
+    }
+}
+
+}  // namespace bd

@@ -1,0 +1,285 @@
+"""Step loops on the GPU, with the reference's API.
+
+LongRangeSimulation mirrors brownsim.dynamics.LongRangeSimulation
+(dynamics.py:177-274): constructor (sys, params, rng, tri=None,
+debug_scan=False, collect_flags=False), step() -> StepStats, run(steps,
+on_step) -> list[StepStats], state read-out via .sys / .tri /
+.last_overlap_flags / .step_index.  Each step is two launches on the current
+CUDA stream: the all-pairs force kernel and ONE persistent cooperative
+kernel that runs integrate, the pass-through check, inversion repair,
+Delaunay flips, overlap correction, the joint fixed point and the rollback
+loop entirely on the device (csrc/bd_step.cuh).  The host reads back only
+the StepStats counters.
+
+Extra keyword arguments (not in the reference):
+  force        "long-range" (default), "short-range" or "long+short" -- the
+               composite force models of SURVEY.md §0 (Verlet-list short
+               range, r_cutoff from params), with the triangulation as the
+               overlap neighbour provider in every case;
+  precision    "exact" (bit-identical to the reference) or "fast" (FMA +
+               rsqrt all-pairs, |dF|/|F| ~1e-12);
+  skin         Verlet skin for the short-range force (default sigma/2).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from ._lib import check, lib, require_cuda
+from .core import (BrownsimError, CounterRng, NonConvergenceError, ParticleSystem, SimParams,
+                   SingularityError, StepFailure)
+from .triangulation import TRI_KEYS, PeriodicTriangulation
+
+RESOLVE_FRAC = 1.0 - 1e-9  # dynamics.py:39
+
+FORCE_MODES = {"long-range": _abi.BD_FORCE_LR, "short-range": _abi.BD_FORCE_SR,
+               "long+short": _abi.BD_FORCE_LRSR}
+PRECISIONS = {"exact": _abi.BD_LR_EXACT, "fast": _abi.BD_LR_FAST}
+
+
+@dataclass
+class StepStats:
+    """Per-step counters and phase timings (dynamics.py:42-57)."""
+
+    step: int
+    dt_used: float
+    overlap_iterations: int = 0
+    flip_passes: int = 0
+    inversion_repairs: int = 0
+    rollbacks: int = 0
+    n_overlapping: int = 0
+    force_ms: float = 0.0
+    maintain_ms: float = 0.0
+    overlap_ms: float = 0.0
+    step_ms: float = 0.0
+    overlap_flags: np.ndarray | None = field(default=None, repr=False)
+
+
+class MissedOverlapError(BrownsimError):
+    """Debug scan found an overlapping pair the neighbour provider missed."""
+
+
+def _tri_struct(tensors: dict, nv: int) -> _abi.BdTri:
+    return _abi.BdTri(nv, int(tensors["edge_v"].shape[0]), int(tensors["tri_v"].shape[0]),
+                      *[tensors[k].data_ptr() for k in TRI_KEYS])
+
+
+def _stream():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def make_params(params: SimParams, box_length: float, seed: int, stream: int, force_mode: int = 0,
+                precision: int = 0, skin: float | None = None) -> _abi.BdParams:
+    p = _abi.BdParams()
+    p.n = params.n
+    p.L = float(box_length)
+    p.sigma, p.dt, p.diffusion = float(params.sigma), float(params.dt), float(params.diffusion)
+    p.cap, p.clamp = float(params.displacement_cap), float(params.noise_clamp)
+    p.r_cut = float(params.r_cutoff) if params.r_cutoff is not None else 0.0
+    p.skin = 0.5 * params.sigma if skin is None else float(skin)
+    p.tol = 1e-12
+    p.max_overlap_iters, p.max_rollbacks = int(params.max_overlap_iters), int(params.max_rollbacks)
+    p.seed, p.stream = int(seed) & ((1 << 64) - 1), int(stream) & ((1 << 64) - 1)
+    p.force_mode, p.lr_precision = int(force_mode), int(precision)
+    lib().bd_prepare_params(ctypes.byref(p))
+    return p
+
+
+class _Engine:
+    """Device buffers + the C-ABI state struct of one simulation."""
+
+    def __init__(self, sys: ParticleSystem, tri: PeriodicTriangulation | None, bparams: _abi.BdParams, call: int):
+        torch = require_cuda()
+        dev = sys.device
+        n = sys.n
+        self.sys, self.tri, self.p = sys, tri, bparams
+        self.force_err = torch.zeros(n, dtype=torch.int64, device=dev)
+        self.overlap_flags = torch.zeros(n, dtype=torch.uint8, device=dev)
+        self.call_t = torch.tensor([call], dtype=torch.int64, device=dev)
+        self.stats_t = torch.zeros(_abi.STATS_WORDS, dtype=torch.int64, device=dev)
+        ne = tri.n_edges if tri is not None else 0
+        nt = tri.n_triangles if tri is not None else 0
+        wb = lib().bd_workspace_bytes(n, ne, nt, int(bparams.pair_capacity))
+        self.work = torch.zeros(wb // 8 + 64, dtype=torch.int64, device=dev)
+        s = _abi.BdState()
+        s.pos, s.prev, s.force = sys.positions_t.data_ptr(), sys.positions_prev_t.data_ptr(), sys.forces_t.data_ptr()
+        s.alpha, s.mu = sys.alpha_t.data_ptr(), sys.mu_t.data_ptr()
+        s.force_err = self.force_err.data_ptr()
+        s.image = sys.image_t.data_ptr()
+        s.overlap_flags = self.overlap_flags.data_ptr()
+        if tri is not None:
+            s.tri = _tri_struct(tri.tensors(), n)
+            s.tri_backup = _tri_struct(tri.backup_tensors(), n)
+        s.call = self.call_t.data_ptr()
+        s.stats = self.stats_t.data_ptr()
+        s.work = self.work.data_ptr()
+        s.work_bytes = self.work.numel() * 8
+        self.s = s
+
+    def clear_status(self):
+        check(lib().bd_clear_status(ctypes.byref(self.s), _stream()), "bd_clear_status")
+
+
+def _raise_for(st: dict, step_index: int):
+    code = int(st["status"])
+    if code == _abi.BD_OK:
+        return
+    if code == _abi.BD_ERR_SINGULAR:
+        raise SingularityError(f"particles {st['err_i']} and {st['err_k']} at zero separation")
+    if code == _abi.BD_ERR_NONCONV:
+        raise NonConvergenceError(f"step {step_index}: iterative procedure exceeded its iteration cap")
+    if code == _abi.BD_ERR_STEPFAIL:
+        raise StepFailure(f"step {step_index}: non-finite force or rollback budget exhausted "
+                          f"(particle/rollbacks {st['err_i']})")
+    if code == _abi.BD_ERR_FLIP:
+        raise BrownsimError(f"step {step_index}: edge {st['err_i']} not flippable")
+    raise BrownsimError(f"step {step_index}: device status {code}")
+
+
+def _decode_stats(words: np.ndarray) -> dict:
+    raw = _abi.BdStats.from_buffer_copy(np.ascontiguousarray(words, dtype=np.int64).tobytes())
+    return {k: (getattr(raw, k) if k != "reserved" else None) for k, _ in _abi.BdStats._fields_}
+
+
+class _SimulationBase:
+    def __init__(self, sys: ParticleSystem, params: SimParams, rng, debug_scan=False, collect_flags=False):
+        self.sys = sys
+        self.params = params
+        self.rng = rng if rng is not None else CounterRng(0, 2)
+        self.debug_scan = debug_scan
+        self.collect_flags = collect_flags
+        self.step_index = 0
+
+    @property
+    def last_overlap_flags(self) -> np.ndarray:
+        return self._eng.overlap_flags.cpu().numpy().astype(bool)
+
+    def _sync_rng(self):
+        self.rng.call = int(self._eng.call_t.item())
+
+
+def device_restore_delaunay(tri: PeriodicTriangulation, positions, box, tol=1e-12) -> int:
+    """restore_delaunay (triangulation.py:319-334) on the GPU for a host position array."""
+    torch = require_cuda()
+    pos_np = np.ascontiguousarray(positions, dtype=np.float64)
+    n = pos_np.shape[0]
+    sys = ParticleSystem.__new__(ParticleSystem)
+    dev = tri.device
+    sys.box, sys.device = box, dev
+    sys.positions_t = torch.from_numpy(pos_np).to(dev)
+    sys.positions_prev_t = sys.positions_t.clone()
+    sys.forces_t = torch.zeros_like(sys.positions_t)
+    sys.alpha_t = torch.zeros(n, dtype=torch.float64, device=dev)
+    sys.mu_t = torch.zeros(n, dtype=torch.float64, device=dev)
+    sys.image_t = torch.zeros((n, 2), dtype=torch.int32, device=dev)
+    params = SimParams(n=n, sigma=1.0, dt=0.01, diffusion=0.0)
+    bp = make_params(params, box.length, 0, 0)
+    bp.tol = float(tol)
+    eng = _Engine(sys, tri, bp, 0)
+    out = torch.zeros(1, dtype=torch.int64, device=dev)
+    check(lib().bd_tri_restore_delaunay(ctypes.byref(eng.s), ctypes.byref(bp), ctypes.c_void_p(out.data_ptr()),
+                                        _stream()), "bd_tri_restore_delaunay")
+    passes = int(out.item())
+    if passes < 0:
+        raise NonConvergenceError("delaunay restoration did not converge")
+    return passes
+
+
+class LongRangeSimulation(_SimulationBase):
+    """All-pairs forces with a continuously maintained triangulation
+    (dynamics.py:177-274), every phase on the GPU."""
+
+    def __init__(self, sys: ParticleSystem, params: SimParams, rng=None, tri: PeriodicTriangulation | None = None,
+                 debug_scan: bool = False, collect_flags: bool = False, force: str = "long-range",
+                 precision: str = "exact", skin: float | None = None):
+        super().__init__(sys, params, rng, debug_scan, collect_flags)
+        if tri is None:
+            from .triangulation import build_initial
+            tri = build_initial(sys.positions, sys.box, device=sys.device)
+        self.tri = tri
+        if force not in FORCE_MODES:
+            raise BrownsimError(f"unknown force model {force!r}; have {sorted(FORCE_MODES)}")
+        if force != "long-range" and params.r_cutoff is None:
+            raise BrownsimError("short-range force requires params.r_cutoff")
+        if precision not in PRECISIONS:
+            raise BrownsimError(f"unknown precision {precision!r}; have {sorted(PRECISIONS)}")
+        self.force_model = force
+        self.precision = precision
+        self.bparams = make_params(params, sys.box.length, self.rng.seed, self.rng.stream, FORCE_MODES[force],
+                                   PRECISIONS[precision], skin)
+        self._eng = _Engine(sys, tri, self.bparams, self.rng.call)
+        self._eng.clear_status()
+
+    def _refresh_params(self):
+        # the reference lets tests mutate sim.params between steps (e.g. dt)
+        p = self.params
+        b = self.bparams
+        b.dt, b.diffusion = float(p.dt), float(p.diffusion)
+        b.max_overlap_iters, b.max_rollbacks = int(p.max_overlap_iters), int(p.max_rollbacks)
+        b.cap, b.clamp = float(p.displacement_cap), float(p.noise_clamp)
+
+    def _launch_step(self, stats_ptr: int):
+        L = lib()
+        check(L.bd_force(ctypes.byref(self._eng.s), ctypes.byref(self.bparams), _stream()), "bd_force")
+        check(L.bd_maintain_tri(ctypes.byref(self._eng.s), ctypes.byref(self.bparams), ctypes.c_void_p(stats_ptr),
+                                _stream()), "bd_maintain_tri")
+
+    def step(self) -> StepStats:
+        return self.run(1)[0]
+
+    def run(self, steps: int, on_step=None) -> list:
+        """`steps` steps; without on_step/debug_scan they are queued back to
+        back with a single host synchronisation at the end."""
+        import torch
+        self._refresh_params()
+        if steps <= 0:
+            return []
+        per_step_host = on_step is not None or self.debug_scan or self.collect_flags
+        out = []
+        if per_step_host:
+            for _ in range(steps):
+                out.extend(self._run_batch(1))
+                if self.debug_scan:
+                    from .validation import debug_overlap_scan
+                    debug_overlap_scan(self.sys, self.params)
+                if on_step is not None:
+                    on_step(self, out[-1])
+            return out
+        return self._run_batch(steps)
+
+    def _run_batch(self, steps: int) -> list:
+        import torch
+        stats = torch.zeros((steps, _abi.STATS_WORDS), dtype=torch.int64, device=self.sys.device)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps + 1)]
+        evs[0].record()
+        for j in range(steps):
+            L = lib()
+            check(L.bd_force(ctypes.byref(self._eng.s), ctypes.byref(self.bparams), _stream()), "bd_force")
+            evs[2 * j + 1].record()
+            check(L.bd_maintain_tri(ctypes.byref(self._eng.s), ctypes.byref(self.bparams),
+                                    ctypes.c_void_p(stats[j].data_ptr()), _stream()), "bd_maintain_tri")
+            evs[2 * j + 2].record()
+        host = stats.cpu().numpy()
+        self._sync_rng()
+        res = []
+        for j in range(steps):
+            st = _decode_stats(host[j])
+            if st["status"] == -1:
+                break
+            force_ms = evs[2 * j].elapsed_time(evs[2 * j + 1])
+            maint_ms = evs[2 * j + 1].elapsed_time(evs[2 * j + 2])
+            _raise_for(st, self.step_index)
+            flags = self.last_overlap_flags.copy() if self.collect_flags else None
+            res.append(StepStats(step=self.step_index, dt_used=st["dt_used"],
+                                 overlap_iterations=st["overlap_iterations"], flip_passes=st["flip_passes"],
+                                 inversion_repairs=st["inversion_repairs"], rollbacks=st["rollbacks"],
+                                 n_overlapping=st["n_overlapping"], force_ms=force_ms, maintain_ms=maint_ms,
+                                 overlap_ms=0.0, step_ms=force_ms + maint_ms, overlap_flags=flags))
+            self.step_index += 1
+        return res
