@@ -270,7 +270,7 @@ def run_ours(args):
                      "kernel": "k_lr_tiled (all-pairs force)", "flops_per_pair": FLOPS_PER_PAIR},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": args.steps * (4 if args.precision == "fast" else 3),
+        "gpu_launches": args.steps * (9 if args.precision == "fast" else 3),
         "clocks": clk.summary(),
         "audit_ok": bool(rep.ok),
         "setup_s": t_setup,

@@ -99,7 +99,7 @@ typedef struct bd_state {
     int64_t* pair_a;
     int64_t* pair_b;
     double* vl_snap;
-    int64_t* vl_meta; /* [0]=n_pairs, [1]=valid, [2]=rebuilds total */
+    int64_t* vl_meta; /* [0]=n_pairs, [1]=valid, [2]=rebuilds total, [3]=overlap candidates */
     void* work;       /* scratch of bd_workspace_bytes() bytes */
     int64_t work_bytes;
 } bd_state_t;
@@ -107,8 +107,13 @@ typedef struct bd_state {
 /* fills p->mi_lo/mi_hi (and r_list/ncx) from p->L etc.; host-only helper */
 void bd_prepare_params(bd_params_t* p);
 
-/* scratch bytes needed for n particles / ne edges / nt triangles / pair capacity */
-int64_t bd_workspace_bytes(int64_t n, int64_t ne, int64_t nt, int64_t pair_capacity);
+/* scratch bytes of a simulation state: p (after bd_prepare_params: n, ncx,
+ * pair_capacity) with ne edges / nt triangles (0, 0 without a triangulation) */
+int64_t bd_workspace_bytes(const bd_params_t* p, int64_t ne, int64_t nt);
+
+/* scratch bytes of the standalone pair-list entry points below
+ * (bd_verlet_build, bd_short_range_forces, bd_overlap_pass) */
+int64_t bd_pairs_workspace_bytes(int64_t n, double L, double r_list, int64_t n_pairs);
 
 /* ---- kernel boundary (replaces brownsim._kernels) -------------------- */
 
@@ -138,12 +143,12 @@ int bd_overlap_pass(const double* pos, int64_t n, const int64_t* pair_a, const i
 int bd_max_sq_displacement(const double* pos, const double* snap, int64_t n, double L, double* out,
                            void* stream);
 
+
 /* build_cell_grid + cell_pairs (forces.py:81-99, _kernels.py:141-236):
  * ordered Verlet pair list identical to the reference's; writes count[0]
  * (pairs are written only when count <= capacity). */
 int bd_verlet_build(const double* pos, int64_t n, double L, double r_list, int64_t* pair_a,
-                    int64_t* pair_b, int64_t capacity, int64_t* count, void* work,
-                    int64_t work_bytes, void* stream);
+                    int64_t* pair_b, int64_t capacity, int64_t* count, void* work, void* stream);
 
 /* counter-based normals for pairs [0, n_pairs) of one call */
 int bd_normals(uint64_t seed, uint64_t stream_id, uint64_t call, uint64_t purpose, int64_t n_pairs,
@@ -171,8 +176,14 @@ int bd_step_tri(const bd_state_t* s, const bd_params_t* p, void* stream);
 int bd_run_tri(const bd_state_t* s, const bd_params_t* p, int64_t steps, bd_stats_t* stats_out,
                void* stream);
 
-/* one ShortRangeSimulation.step (dynamics.py:326-346) */
+/* one ShortRangeSimulation.step (dynamics.py:326-346): Verlet list kept
+ * fresh on device, short-range force, integrate, overlap rounds over the
+ * overlap candidates with rebuilds -- one persistent kernel */
 int bd_step_verlet(const bd_state_t* s, const bd_params_t* p, bd_stats_t* stats_out, void* stream);
+
+/* `steps` consecutive ShortRangeSimulation steps (stats_out[j], device) */
+int bd_run_verlet(const bd_state_t* s, const bd_params_t* p, int64_t steps, bd_stats_t* stats_out,
+                  void* stream);
 
 /* restore_delaunay (triangulation.py:319-334) on the state's triangulation
  * and positions; passes (or -1 on error) written to passes_out[0] (device) */

@@ -63,15 +63,16 @@ def _protos():
     P = ctypes.POINTER
     return {
         "bd_prepare_params": ([P(BdParams)], None),
-        "bd_workspace_bytes": ([c_i64, c_i64, c_i64, c_i64], c_i64),
+        "bd_workspace_bytes": ([P(BdParams), c_i64, c_i64], c_i64),
+        "bd_pairs_workspace_bytes": ([c_i64, c_d, c_d, c_i64], c_i64),
         "bd_long_range_workspace_bytes": ([c_i64], c_i64),
         "bd_long_range_forces": ([c_vp, c_vp, c_vp, c_i64, c_d, c_i64, c_i64, c_int, c_vp, c_vp, c_vp, c_vp], c_int),
         "bd_short_range_forces": ([c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_d, c_d, c_vp, c_vp, c_vp, c_vp],
                                   c_int),
         "bd_overlap_pass": ([c_vp, c_i64, c_vp, c_vp, c_i64, c_d, c_d, c_d, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
         "bd_max_sq_displacement": ([c_vp, c_vp, c_i64, c_d, c_vp, c_vp], c_int),
-        "bd_verlet_build": ([c_vp, c_i64, c_d, c_d, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp], c_int),
-        "bd_verlet_workspace_bytes": ([c_i64, c_d, c_d], c_i64),
+        "bd_verlet_build": ([c_vp, c_i64, c_d, c_d, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp], c_int),
+        "bd_probe_fp64": ([c_i64, c_vp, c_vp, P(c_d)], c_int),
         "bd_normals": ([c_u64, c_u64, c_u64, c_u64, c_i64, c_vp, c_vp], c_int),
         "bd_force": ([P(BdState), P(BdParams), c_vp], c_int),
         "bd_maintain_tri": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
@@ -99,6 +100,6 @@ def declare(lib):
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = ("bd_force", "bd_maintain_tri", "bd_prepare_params", "bd_workspace_bytes", "bd_long_range_workspace_bytes",
            "bd_long_range_forces", "bd_short_range_forces", "bd_overlap_pass",
-           "bd_max_sq_displacement", "bd_verlet_build", "bd_verlet_workspace_bytes", "bd_normals",
+           "bd_max_sq_displacement", "bd_verlet_build", "bd_pairs_workspace_bytes", "bd_normals",
            "bd_step_tri", "bd_run_tri", "bd_step_verlet", "bd_run_verlet",
            "bd_tri_restore_delaunay", "bd_clear_status", "bd_tri_audit_geometry", "bd_build_info")

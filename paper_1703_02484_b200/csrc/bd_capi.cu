@@ -1,27 +1,27 @@
 // bd_capi.cu -- extern "C" entry points of libbd_b200.so (include/bd_b200.h).
 //
-// Host side only launches: every loop of the step runs inside the
-// persistent step kernel (bd_step.cuh) or the all-pairs kernel
-// (bd_allpairs.cuh).  No entry point allocates device memory or
-// synchronises the host.
+// Host side only launches: every loop of a step runs inside the persistent
+// step kernels (bd_drivers.cuh, one source for the cooperative-grid and the
+// single-CTA variants) or the all-pairs kernels (bd_allpairs*.cuh).  No
+// entry point allocates device memory or synchronises the host.
 #include <cuda_runtime.h>
 
 #include <mutex>
 
 #include "bd_allpairs.cuh"
-#include "bd_step.cuh"
+#include "bd_drivers.cuh"
 
 using namespace bd;
 
 namespace {
 
-constexpr int LR_BT = 128;  // receivers per CTA of the all-pairs kernel
-constexpr int LR_TS = 512;  // sources per smem stage (2 stages x 16 KiB)
 constexpr int STEP_BT = 256;
 constexpr int BLOCK_BT = 1024;
 
 int g_num_sms = 0;
 int g_grid_blocks_per_sm = 0;
+int g_lr_blocks_per_sm[2] = {1, 1};
+int g_fast_blocks_per_sm = 1;
 std::once_flag g_once;
 
 int64_t block_max_n() {
@@ -33,24 +33,38 @@ int64_t block_max_n() {
     return v;
 }
 
-__global__ void __launch_bounds__(STEP_BT) k_step_tri_grid(bd_state_t s, bd_params_t p, bd_stats_t* out) {
+BD_DEV Ctx make_ctx(const bd_state_t& s, const bd_params_t& p) {
     Ctx c;
     c.p = p;
     c.s = s;
-    c.w = ws_carve(s.work, p.n, s.tri.ne, s.tri.nt);
-    c.call = *s.call;
+    c.w = ws_carve(s.work, p, s.tri.ne, s.tri.nt);
+    c.call = s.call ? *s.call : 0;
+    return c;
+}
+
+// ---- persistent drivers: cooperative grid (barrier = grid.sync) and one CTA
+__global__ void __launch_bounds__(STEP_BT) k_step_tri_grid(bd_state_t s, bd_params_t p, bd_stats_t* out) {
+    Ctx c = make_ctx(s, p);
     ExecGrid x{c.w.ctl};
     step_tri_after_force(x, c, out);
 }
 
 __global__ void __launch_bounds__(BLOCK_BT) k_step_tri_block(bd_state_t s, bd_params_t p, bd_stats_t* out) {
-    Ctx c;
-    c.p = p;
-    c.s = s;
-    c.w = ws_carve(s.work, p.n, s.tri.ne, s.tri.nt);
-    c.call = *s.call;
+    Ctx c = make_ctx(s, p);
     ExecBlock x{c.w.ctl};
     step_tri_after_force(x, c, out);
+}
+
+__global__ void __launch_bounds__(STEP_BT) k_step_verlet_grid(bd_state_t s, bd_params_t p, bd_stats_t* out) {
+    Ctx c = make_ctx(s, p);
+    ExecGrid x{c.w.ctl};
+    step_verlet(x, c, out);
+}
+
+__global__ void __launch_bounds__(BLOCK_BT) k_step_verlet_block(bd_state_t s, bd_params_t p, bd_stats_t* out) {
+    Ctx c = make_ctx(s, p);
+    ExecBlock x{c.w.ctl};
+    step_verlet(x, c, out);
 }
 
 template <class X>
@@ -64,13 +78,102 @@ __device__ void restore_delaunay_entry(X& x, Ctx& c, int64_t* passes_out) {
 }
 
 __global__ void __launch_bounds__(STEP_BT) k_restore_delaunay_grid(bd_state_t s, bd_params_t p, int64_t* out) {
-    Ctx c;
-    c.p = p;
-    c.s = s;
-    c.w = ws_carve(s.work, p.n, s.tri.ne, s.tri.nt);
-    c.call = 0;
+    Ctx c = make_ctx(s, p);
     ExecGrid x{c.w.ctl};
     restore_delaunay_entry(x, c, out);
+}
+
+// ---- kernel-boundary drop-ins over pair lists (cooperative grid) ----------
+
+// build_cell_grid + cell_pairs (+ snapshot) into pair_a/pair_b; count[0]
+__global__ void __launch_bounds__(STEP_BT) k_verlet_build_grid(bd_state_t s, bd_params_t p, int64_t* count) {
+    Ctx c = make_ctx(s, p);
+    ExecGrid x{c.w.ctl};
+    Red<ExecGrid> R(x);
+    if (x.leader()) {
+        for (int k = 0; k < 8; ++k) c.w.ctl->red[k] = 0;
+        c.w.ctl->status = 0;
+        c.s.vl_meta[1] = 0;
+    }
+    x.sync();
+    const bool ok = vl_rebuild(x, R, c, 0.0);
+    if (x.leader()) count[0] = ok ? c.s.vl_meta[0] : (int64_t)c.w.ctl->err_i;
+}
+
+// short_range_kernel over a given pair list
+__global__ void __launch_bounds__(STEP_BT) k_short_range_grid(bd_state_t s, bd_params_t p, int64_t npairs,
+                                                              double* out, int64_t* err) {
+    Ctx c = make_ctx(s, p);
+    ExecGrid x{c.w.ctl};
+    const ListPairs lp{c.s.pair_a, c.s.pair_b, npairs};
+    build_incidence(x, p.n, lp, c.w.vinc_off, c.w.vinc_cur, c.w.vinc);
+    sr_forces(x, c, out, err);
+}
+
+// overlap_pass_kernel over a given pair list: disp / flags / count (not applied)
+__global__ void __launch_bounds__(STEP_BT) k_overlap_pass_grid(bd_state_t s, bd_params_t p, int64_t npairs,
+                                                               double resolve, double* disp, uint8_t* flags,
+                                                               int64_t* count) {
+    Ctx c = make_ctx(s, p);
+    ExecGrid x{c.w.ctl};
+    Red<ExecGrid> R(x);
+    if (x.leader())
+        for (int k = 0; k < 8; ++k) c.w.ctl->red[k] = 0;
+    x.sync();
+    const ListPairs lp{c.s.pair_a, c.s.pair_b, npairs};
+    build_incidence(x, p.n, lp, c.w.inc_off, c.w.inc_cur, c.w.inc);
+    const double sigma = p.sigma, thresh = sigma * resolve;
+    const double* pos = c.s.pos;
+    u64* r = R.open();
+    for (int64_t e = x.tid(); e < npairs; e += x.nth()) {
+        const int64_t a = lp.a(e), b = lp.b(e);
+        const double dx = mi_exact(pos[2 * b] - pos[2 * a], p), dy = mi_exact(pos[2 * b + 1] - pos[2 * a + 1], p);
+        const double rr = sqrt(dx * dx + dy * dy);
+        const bool ov = !(rr >= thresh || rr == 0.0);
+        if (ov) {
+            const double delta = sigma - rr;
+            c.w.contrib[2 * e] = delta * (dx / rr);
+            c.w.contrib[2 * e + 1] = delta * (dy / rr);
+        }
+        c.w.eovl[e] = (uint8_t)ov;
+        x.add(r, (u64)ov);
+    }
+    const u64 cnt = R.close(r);
+    for (int64_t i = x.tid(); i < p.n; i += x.nth()) {
+        double dx = 0.0, dy = 0.0;
+        bool hit = false;
+        for (int32_t j = c.w.inc_off[i]; j < c.w.inc_off[i + 1]; ++j) {
+            const int64_t e = c.w.inc[j];
+            if (!c.w.eovl[e]) continue;
+            hit = true;
+            if (lp.a(e) == i) {
+                dx -= c.w.contrib[2 * e];
+                dy -= c.w.contrib[2 * e + 1];
+            } else {
+                dx += c.w.contrib[2 * e];
+                dy += c.w.contrib[2 * e + 1];
+            }
+        }
+        disp[2 * i] = dx;
+        disp[2 * i + 1] = dy;
+        flags[i] = hit;
+    }
+    if (x.leader()) count[0] = (int64_t)cnt;
+}
+
+__global__ void k_max_sq_disp(const double* pos, const double* snap, int64_t n, bd_params_t p, unsigned long long* out) {
+    unsigned long long best = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double dx = mi_exact(pos[2 * i] - snap[2 * i], p), dy = mi_exact(pos[2 * i + 1] - snap[2 * i + 1], p);
+        const unsigned long long b = (unsigned long long)__double_as_longlong(dx * dx + dy * dy);
+        best = b > best ? b : best;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(0xffffffffu, best, o);
+        best = v > best ? v : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
 }
 
 __global__ void k_normals(uint64_t seed, uint64_t stream_id, uint64_t call, uint64_t purpose, int64_t npairs,
@@ -118,21 +221,29 @@ __global__ void k_probe_fp64(int64_t iters, double* out) {
     out[tid & ((1 << 20) - 1)] = s;
 }
 
+int occupancy(const void* f, int bt) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, bt, 0);
+    return nb > 0 ? nb : 1;
+}
+
 void init_device_info() {
     std::call_once(g_once, [] {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        int nb = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_step_tri_grid, STEP_BT, 0);
-        int nb2 = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, k_restore_delaunay_grid, STEP_BT, 0);
-        g_grid_blocks_per_sm = nb < nb2 ? nb : nb2;
-        if (g_grid_blocks_per_sm < 1) g_grid_blocks_per_sm = 1;
-        cudaFuncSetAttribute(k_lr_tiled<false, LR_BT, LR_TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             2 * LR_TS * 32);
-        cudaFuncSetAttribute(k_lr_tiled<true, LR_BT, LR_TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             2 * LR_TS * 32);
+        int m = occupancy((const void*)k_step_tri_grid, STEP_BT);
+        const void* coop[] = {(const void*)k_restore_delaunay_grid, (const void*)k_step_verlet_grid,
+                              (const void*)k_verlet_build_grid, (const void*)k_short_range_grid,
+                              (const void*)k_overlap_pass_grid};
+        for (const void* f : coop) {
+            const int o = occupancy(f, STEP_BT);
+            m = o < m ? o : m;
+        }
+        g_grid_blocks_per_sm = m;
+        g_lr_blocks_per_sm[1] = occupancy((const void*)k_allpairs<true>, LR_BT);
+        g_lr_blocks_per_sm[0] = occupancy((const void*)k_allpairs<false>, LR_BT);
+        g_fast_blocks_per_sm = occupancy((const void*)k_allpairs_fast, FS_BT);
     });
 }
 
@@ -146,53 +257,112 @@ int grid_blocks(int64_t work_items) {
 
 int err_code(cudaError_t e) { return e == cudaSuccess ? 0 : -(int)e; }
 
+unsigned grid_for(int64_t items, int bt = 256) {
+    int64_t nb = (items + bt - 1) / bt;
+    if (nb > 8 * (int64_t)g_num_sms) nb = 8 * (int64_t)g_num_sms;
+    return (unsigned)(nb < 1 ? 1 : nb);
+}
+
+int coop_launch(const void* f, int64_t items, void** args, cudaStream_t st) {
+    return err_code(cudaLaunchCooperativeKernel(f, dim3(grid_blocks(items)), dim3(STEP_BT), args, 0, st));
+}
+
+// ---- all-pairs launches ------------------------------------------------------
+
+// EXACT (and unsorted FAST for receiver sub-ranges): one wave of equally
+// loaded CTAs, 148 x m CTAs, m the smallest multiple of SMs holding every
+// receiver at <= LR_BT per CTA (more waves only past the residency limit)
 int launch_lr(const double4* src, const double* mu, int64_t n, const bd_params_t& p, int64_t i0, int64_t i1,
               int precision, double* out, int64_t* err, cudaStream_t st) {
     if (i1 <= i0) return 0;
-    const int64_t nb = (i1 - i0 + LR_BT - 1) / LR_BT;
-    const size_t smem = 2 * LR_TS * 32;
-    if (precision == BD_LR_FAST) {
-        k_lr_tiled<true, LR_BT, LR_TS><<<(unsigned)nb, LR_BT, smem, st>>>(src, mu, n, p.L, p.mi_lo, p.mi_hi, i0, i1,
-                                                                          out, err);
-        k_lr_rescan<<<(unsigned)((i1 - i0 + 255) / 256 < 1184 ? (i1 - i0 + 255) / 256 : 1184), 256, 0, st>>>(
-            src, n, p.L, p.mi_lo, p.mi_hi, i0, i1, err);
+    const int fast = precision == BD_LR_FAST;
+    const int64_t R = i1 - i0;
+    const int64_t nb_min = (R + LR_BT - 1) / LR_BT;
+    const int64_t m = (nb_min + g_num_sms - 1) / g_num_sms;
+    int64_t nb = m <= g_lr_blocks_per_sm[fast] ? (int64_t)g_num_sms * m : nb_min;
+    if (nb > R) nb = R;
+    const int64_t per_block = (R + nb - 1) / nb;
+    nb = (R + per_block - 1) / per_block;
+    if (fast) {
+        k_allpairs<true><<<(unsigned)nb, LR_BT, 0, st>>>(src, mu, n, p.L, p.mi_lo, p.mi_hi, i0, i1, per_block, out,
+                                                           err);
+        k_lr_rescan<<<grid_for(R), 256, 0, st>>>(src, n, p.L, p.mi_lo, p.mi_hi, i0, i1, err);
     } else {
-        k_lr_tiled<false, LR_BT, LR_TS><<<(unsigned)nb, LR_BT, smem, st>>>(src, mu, n, p.L, p.mi_lo, p.mi_hi, i0,
-                                                                           i1, out, err);
+        k_allpairs<false><<<(unsigned)nb, LR_BT, 0, st>>>(src, mu, n, p.L, p.mi_lo, p.mi_hi, i0, i1, per_block, out,
+                                                            err);
     }
     return err_code(cudaGetLastError());
 }
 
 int launch_pack(const double* pos, const double* alpha, int64_t n, double4* src, cudaStream_t st) {
-    int64_t nb = (n + 255) / 256;
-    if (nb > 4096) nb = 4096;
-    if (nb < 1) nb = 1;
-    k_pack_sources<<<(unsigned)nb, 256, 0, st>>>(pos, alpha, n, src);
+    k_pack_sources<<<grid_for(n), 256, 0, st>>>(pos, alpha, n, src);
+    return err_code(cudaGetLastError());
+}
+
+// FAST stage 1: Morton counting sort + 48-byte source packing + tile boxes
+int launch_fast_prepare(const double* pos, const double* alpha, const double* mu, int64_t n, double L,
+                        const SortWs& w, cudaStream_t st) {
+    const int64_t nc = fast_ncells(n);
+    cudaError_t e = cudaMemsetAsync(w.cell_off, 0, sizeof(int32_t) * (nc + 1), st);
+    if (e != cudaSuccess) return err_code(e);
+    k_sort_count<<<grid_for(n), 256, 0, st>>>(pos, n, L, w);
+    k_sort_scan<<<1, 1024, 0, st>>>(w, nc);
+    k_sort_scatter<<<grid_for(n), 256, 0, st>>>(n, w);
+    k_sort_fix<<<grid_for(nc), 256, 0, st>>>(nc, w);
+    k_pack6<<<(unsigned)((n + FS_TS - 1) / FS_TS), FS_TS, 0, st>>>(pos, alpha, mu, n, w);
+    return err_code(cudaGetLastError());
+}
+
+// FAST stage 2: receivers = sorted slots [s0, s1)
+int launch_fast_slots(int64_t n, const bd_params_t& p, int64_t s0, int64_t s1, const SortWs& w, cudaStream_t st) {
+    if (s1 <= s0) return 0;
+    const int64_t nb = (s1 - s0 + FS_RPB - 1) / FS_RPB;
+    k_allpairs_fast<<<(unsigned)nb, FS_BT, 0, st>>>(w, n, p.L, p.mi_lo, p.mi_hi, s0, s1);
+    return err_code(cudaGetLastError());
+}
+
+// FAST stage 3: slots -> particle order; exact re-scan of flagged receivers
+int launch_fast_finish(const double* pos, int64_t n, const bd_params_t& p, const SortWs& w, double* out,
+                       int64_t* err, cudaStream_t st) {
+    k_unsort_forces<<<grid_for(n), 256, 0, st>>>(0, n, w, out, err);
+    k_lr_rescan_pos<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, p.mi_lo, p.mi_hi, err);
     return err_code(cudaGetLastError());
 }
 
 int launch_force(const bd_state_t* s, const bd_params_t* p, cudaStream_t st) {
     init_device_info();
-    const Ws w = ws_carve(s->work, p->n, s->tri.ne, s->tri.nt);
+    if (p->force_mode == BD_FORCE_SR) return 0;  // the short-range force runs inside the step kernel
+    const Ws w = ws_carve(s->work, *p, s->tri.ne, s->tri.nt);
     // force on the pre-move positions (dynamics.py:194)
+    if (p->lr_precision == BD_LR_FAST) {
+        const SortWs fw = fast_ws_carve(w.src4, p->n);
+        int rc = launch_fast_prepare(s->pos, s->alpha, s->mu, p->n, p->L, fw, st);
+        if (rc) return rc;
+        rc = launch_fast_slots(p->n, *p, 0, p->n, fw, st);
+        if (rc) return rc;
+        return launch_fast_finish(s->pos, p->n, *p, fw, s->force, s->force_err, st);
+    }
     int rc = launch_pack(s->pos, s->alpha, p->n, (double4*)w.src4, st);
     if (rc) return rc;
     return launch_lr((const double4*)w.src4, s->mu, p->n, *p, 0, p->n, (int)p->lr_precision, s->force,
                      s->force_err, st);
 }
 
-int launch_maintain_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
+int launch_driver(const void* grid_fn, const void* block_fn, const bd_state_t* s, const bd_params_t* p,
+                  bd_stats_t* out, cudaStream_t st) {
     init_device_info();
     bd_state_t sv = *s;
     bd_params_t pv = *p;
-    if (p->n <= block_max_n()) {
-        k_step_tri_block<<<1, BLOCK_BT, 0, st>>>(sv, pv, out);
-        return err_code(cudaGetLastError());
-    }
-    const int64_t items = s->tri.ne > p->n ? s->tri.ne : p->n;
     void* args[] = {&sv, &pv, &out};
-    return err_code(cudaLaunchCooperativeKernel((const void*)k_step_tri_grid, dim3(grid_blocks(items)), dim3(STEP_BT),
-                                                args, 0, st));
+    if (p->n <= block_max_n())
+        return err_code(cudaLaunchKernel(block_fn, dim3(1), dim3(BLOCK_BT), args, 0, st));
+    int64_t items = s->tri.ne > p->n ? s->tri.ne : p->n;
+    if (p->pair_capacity > items) items = p->pair_capacity;
+    return coop_launch(grid_fn, items, args, st);
+}
+
+int launch_maintain_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
+    return launch_driver((const void*)k_step_tri_grid, (const void*)k_step_tri_block, s, p, out, st);
 }
 
 int launch_step_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
@@ -201,18 +371,66 @@ int launch_step_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, 
     return launch_maintain_tri(s, p, out, st);
 }
 
+int launch_step_verlet(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
+    return launch_driver((const void*)k_step_verlet_grid, (const void*)k_step_verlet_block, s, p, out, st);
+}
+
+// a transient state for the standalone pair-list entry points
+struct PairCtx {
+    bd_params_t p;
+    bd_state_t s;
+    int64_t meta[4];
+};
+
+bool pair_ctx(PairCtx& pc, const double* pos, int64_t n, double L, double r_list, int64_t capacity, void* work) {
+    memset(&pc, 0, sizeof(pc));
+    pc.p.n = n;
+    pc.p.L = L;
+    pc.p.sigma = 1.0;
+    pc.p.skin = 0.0;
+    pc.p.r_cut = r_list;
+    prepare_params(&pc.p);
+    pc.p.r_list = r_list;
+    const int64_t ncx = (int64_t)floor(L / r_list);
+    pc.p.ncx = ncx < 3 ? 0 : ncx;
+    pc.p.pair_capacity = capacity > 0 ? capacity : 1;
+    const WsLayout l = ws_layout(pc.p, 0, 0);
+    char* b = (char*)work;
+    pc.s.pos = (double*)pos;
+    pc.s.work = b;
+    pc.s.work_bytes = l.total;
+    pc.s.vl_snap = (double*)(b + l.total);
+    pc.s.vl_meta = (int64_t*)(b + l.total + align_up(16 * n));
+    return true;
+}
+
+int64_t pair_ws_bytes(int64_t n, double L, double r_list, int64_t n_pairs) {
+    PairCtx pc;
+    memset(&pc, 0, sizeof(pc));
+    pc.p.n = n;
+    pc.p.L = L;
+    const int64_t ncx = r_list > 0 ? (int64_t)floor(L / r_list) : 0;
+    pc.p.ncx = ncx < 3 ? 0 : ncx;
+    pc.p.pair_capacity = n_pairs > 0 ? n_pairs : 1;
+    return ws_layout(pc.p, 0, 0).total + align_up(16 * n) + 256;
+}
+
 }  // namespace
 
 extern "C" {
 
 void bd_prepare_params(bd_params_t* p) { prepare_params(p); }
 
-int64_t bd_workspace_bytes(int64_t n, int64_t ne, int64_t nt, int64_t pair_capacity) {
-    (void)pair_capacity;
-    return ws_layout(n, ne, nt).total;
+int64_t bd_workspace_bytes(const bd_params_t* p, int64_t ne, int64_t nt) { return ws_layout(*p, ne, nt).total; }
+
+int64_t bd_pairs_workspace_bytes(int64_t n, double L, double r_list, int64_t n_pairs) {
+    return pair_ws_bytes(n, L, r_list, n_pairs);
 }
 
-int64_t bd_long_range_workspace_bytes(int64_t n) { return 32 * n + 256; }
+int64_t bd_long_range_workspace_bytes(int64_t n) {
+    const int64_t f = fast_ws_bytes(n);
+    return (f > 32 * n ? f : 32 * n) + 512;
+}
 
 int bd_long_range_forces(const double* pos, const double* alpha, const double* mu, int64_t n, double L, int64_t i_begin,
                          int64_t i_end, int precision, double* out, int64_t* err, void* work, void* stream) {
@@ -221,18 +439,78 @@ int bd_long_range_forces(const double* pos, const double* alpha, const double* m
     bd_params_t p;
     memset(&p, 0, sizeof(p));
     p.L = L;
-    bd_prepare_params(&p);
+    prepare_params(&p);
+    if (precision == BD_LR_FAST && i_begin == 0 && i_end == n) {
+        const SortWs fw = fast_ws_carve(work, n);
+        int rc = launch_fast_prepare(pos, alpha, mu, n, L, fw, st);
+        if (rc) return rc;
+        rc = launch_fast_slots(n, p, 0, n, fw, st);
+        if (rc) return rc;
+        return launch_fast_finish(pos, n, p, fw, out, err, st);
+    }
     int rc = launch_pack(pos, alpha, n, (double4*)work, st);
     if (rc) return rc;
     return launch_lr((const double4*)work, mu, n, p, i_begin, i_end, precision, out, err, st);
 }
 
+int bd_verlet_build(const double* pos, int64_t n, double L, double r_list, int64_t* pair_a, int64_t* pair_b,
+                    int64_t capacity, int64_t* count, void* work, void* stream) {
+    init_device_info();
+    PairCtx pc;
+    pair_ctx(pc, pos, n, L, r_list, capacity, work);
+    pc.s.pair_a = pair_a;
+    pc.s.pair_b = pair_b;
+    void* args[] = {&pc.s, &pc.p, &count};
+    return coop_launch((const void*)k_verlet_build_grid, n > capacity ? n : capacity, args, (cudaStream_t)stream);
+}
+
+int bd_short_range_forces(const double* pos, const double* alpha, const double* mu, int64_t n, const int64_t* pair_a,
+                          const int64_t* pair_b, int64_t n_pairs, double L, double r_cut, double* out, int64_t* err,
+                          void* work, void* stream) {
+    init_device_info();
+    PairCtx pc;
+    pair_ctx(pc, pos, n, L, 0.0, n_pairs, work);
+    pc.p.ncx = 0;
+    pc.p.r_cut = r_cut;
+    pc.s.alpha = (double*)alpha;
+    pc.s.mu = (double*)mu;
+    pc.s.pair_a = (int64_t*)pair_a;
+    pc.s.pair_b = (int64_t*)pair_b;
+    void* args[] = {&pc.s, &pc.p, &n_pairs, &out, &err};
+    return coop_launch((const void*)k_short_range_grid, n > n_pairs ? n : n_pairs, args, (cudaStream_t)stream);
+}
+
+int bd_overlap_pass(const double* pos, int64_t n, const int64_t* pair_a, const int64_t* pair_b, int64_t n_pairs,
+                    double L, double sigma, double resolve, double* disp, uint8_t* flags, int64_t* count, void* work,
+                    void* stream) {
+    init_device_info();
+    PairCtx pc;
+    pair_ctx(pc, pos, n, L, 0.0, n_pairs, work);
+    pc.p.ncx = 0;
+    pc.p.sigma = sigma;
+    pc.s.pair_a = (int64_t*)pair_a;
+    pc.s.pair_b = (int64_t*)pair_b;
+    void* args[] = {&pc.s, &pc.p, &n_pairs, &resolve, &disp, &flags, &count};
+    return coop_launch((const void*)k_overlap_pass_grid, n > n_pairs ? n : n_pairs, args, (cudaStream_t)stream);
+}
+
+int bd_max_sq_displacement(const double* pos, const double* snap, int64_t n, double L, double* out, void* stream) {
+    init_device_info();
+    bd_params_t p;
+    memset(&p, 0, sizeof(p));
+    p.L = L;
+    prepare_params(&p);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), st);
+    if (e != cudaSuccess) return err_code(e);
+    k_max_sq_disp<<<grid_for(n), 256, 0, st>>>(pos, snap, n, p, (unsigned long long*)out);
+    return err_code(cudaGetLastError());
+}
+
 int bd_normals(uint64_t seed, uint64_t stream_id, uint64_t call, uint64_t purpose, int64_t n_pairs, double* out,
                void* stream) {
-    int64_t nb = (n_pairs + 255) / 256;
-    if (nb > 4096) nb = 4096;
-    if (nb < 1) nb = 1;
-    k_normals<<<(unsigned)nb, 256, 0, (cudaStream_t)stream>>>(seed, stream_id, call, purpose, n_pairs, out);
+    init_device_info();
+    k_normals<<<grid_for(n_pairs), 256, 0, (cudaStream_t)stream>>>(seed, stream_id, call, purpose, n_pairs, out);
     return err_code(cudaGetLastError());
 }
 
@@ -256,9 +534,21 @@ int bd_run_tri(const bd_state_t* s, const bd_params_t* p, int64_t steps, bd_stat
     return 0;
 }
 
+int bd_step_verlet(const bd_state_t* s, const bd_params_t* p, bd_stats_t* stats_out, void* stream) {
+    return launch_step_verlet(s, p, stats_out, (cudaStream_t)stream);
+}
+
+int bd_run_verlet(const bd_state_t* s, const bd_params_t* p, int64_t steps, bd_stats_t* stats_out, void* stream) {
+    for (int64_t j = 0; j < steps; ++j) {
+        int rc = launch_step_verlet(s, p, stats_out + j, (cudaStream_t)stream);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
 int bd_clear_status(const bd_state_t* s, void* stream) {
-    const Ws w = ws_carve(s->work, 0, 0, 0);
-    return err_code(cudaMemsetAsync(&w.ctl->status, 0, 3 * sizeof(unsigned long long), (cudaStream_t)stream));
+    Ctl* ctl = (Ctl*)s->work;  // the control block heads every workspace
+    return err_code(cudaMemsetAsync(&ctl->status, 0, 3 * sizeof(unsigned long long), (cudaStream_t)stream));
 }
 
 int bd_tri_restore_delaunay(const bd_state_t* s, const bd_params_t* p, int64_t* passes_out, void* stream) {
@@ -267,19 +557,15 @@ int bd_tri_restore_delaunay(const bd_state_t* s, const bd_params_t* p, int64_t* 
     bd_params_t pv = *p;
     void* args[] = {&sv, &pv, &passes_out};
     const int64_t items = s->tri.ne > p->n ? s->tri.ne : p->n;
-    return err_code(cudaLaunchCooperativeKernel((const void*)k_restore_delaunay_grid, dim3(grid_blocks(items)),
-                                                dim3(STEP_BT), args, 0, (cudaStream_t)stream));
+    return coop_launch((const void*)k_restore_delaunay_grid, items, args, (cudaStream_t)stream);
 }
 
 int bd_tri_audit_geometry(const bd_state_t* s, const bd_params_t* p, int64_t* out, void* stream) {
+    init_device_info();
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(int64_t), st);
     if (e != cudaSuccess) return err_code(e);
-    int64_t items = s->tri.ne;
-    int64_t nb = (items + 255) / 256;
-    if (nb > 4096) nb = 4096;
-    if (nb < 1) nb = 1;
-    k_audit_geometry<<<(unsigned)nb, 256, 0, st>>>(s->tri, s->pos, p->L, p->tol, (unsigned long long*)out);
+    k_audit_geometry<<<grid_for(s->tri.ne), 256, 0, st>>>(s->tri, s->pos, p->L, p->tol, (unsigned long long*)out);
     return err_code(cudaGetLastError());
 }
 
@@ -294,7 +580,8 @@ int bd_probe_fp64(int64_t iters, double* out, void* stream, double* flops_out) {
 }
 
 const char* bd_build_info(void) {
-    return "libbd_b200: sm_100a, -fmad=false (exact paths), TMA bulk all-pairs, cooperative step kernel";
+    return "libbd_b200: sm_100a, -fmad=false (exact paths), TMA-staged all-pairs (exact + sorted fast), "
+           "persistent cooperative step kernels (triangulation / Verlet)";
 }
 
 }  // extern "C"

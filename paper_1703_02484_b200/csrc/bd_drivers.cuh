@@ -1,0 +1,222 @@
+// bd_drivers.cuh -- whole-step drivers (uniform control flow over phases).
+//
+//   step_tri_after_force : LongRangeSimulation.step (dynamics.py:191-274)
+//                          after the all-pairs force kernel, with the composite
+//                          force models: short-range Verlet force
+//                          alone or added to the long-range force, the
+//                          triangulation being the overlap neighbour provider;
+//   step_verlet          : ShortRangeSimulation.step (dynamics.py:326-346).
+#pragma once
+
+#include "bd_verlet.cuh"
+
+namespace bd {
+
+// first receiver with a non-zero err sentinel -> SingularityError (forces.py:54-58)
+template <class X>
+BD_HD bool check_singular(X& x, Red<X>& R, Ctx& c, const int64_t* err, bd_stats_t* out) {
+    u64* r = R.open();
+    if (x.leader()) c.w.ctl->scratch[1] = ~0ull;
+    x.sync();
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
+        const bool bad = err[i] != 0;
+        if (bad) x.umin(&c.w.ctl->scratch[1], (u64)i);
+        x.add(r, (u64)bad);
+    }
+    if (!R.close(r)) return false;
+    if (x.leader()) {
+        const int64_t i = (int64_t)c.w.ctl->scratch[1];
+        c.w.ctl->status = BD_ERR_SINGULAR;
+        c.w.ctl->err_i = (u64)i;
+        c.w.ctl->err_k = (u64)(err[i] - 1);
+        out->status = BD_ERR_SINGULAR;
+        out->err_i = i;
+        out->err_k = err[i] - 1;
+    }
+    x.sync();
+    return true;
+}
+
+// non-finite force -> StepFailure (integrate, dynamics.py:84-86)
+template <class X>
+BD_HD bool check_finite(X& x, Red<X>& R, Ctx& c, bd_stats_t* out) {
+    u64* r = R.open();
+    if (x.leader()) c.w.ctl->scratch[0] = ~0ull;
+    x.sync();
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
+        const bool bad = !(isfinite(c.s.force[2 * i]) && isfinite(c.s.force[2 * i + 1]));
+        if (bad) x.umin(&c.w.ctl->scratch[0], (u64)i);
+        x.add(r, (u64)bad);
+    }
+    if (!R.close(r)) return false;
+    if (x.leader()) {
+        c.w.ctl->status = BD_ERR_STEPFAIL;
+        c.w.ctl->err_i = c.w.ctl->scratch[0];
+        out->status = BD_ERR_STEPFAIL;
+        out->err_i = (int64_t)c.w.ctl->scratch[0];
+    }
+    x.sync();
+    return true;
+}
+
+template <class X>
+BD_HD bool driver_enter(X& x, Red<X>& R, Ctx& c, bd_stats_t* out) {
+    if (x.leader())
+        for (int k = 0; k < 8; ++k) c.w.ctl->red[k] = 0;
+    x.sync();
+    if (x.ld(&c.w.ctl->status)) {  // an earlier step failed: this one does not run
+        if (x.leader()) out->status = -1;
+        return false;
+    }
+    return true;
+}
+
+// LongRangeSimulation.step after the all-pairs force (dynamics.py:196-274).
+// s.force holds F_LR (force_mode LR / LRSR) from the all-pairs kernel.
+template <class X>
+BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
+    Red<X> R(x);
+    if (!driver_enter(x, R, c, out)) return;
+    const int64_t rebuilds0 = c.s.vl_meta ? c.s.vl_meta[2] : 0;
+    if (c.p.force_mode != BD_FORCE_SR && check_singular(x, R, c, c.s.force_err, out)) return;
+    if (c.p.force_mode != BD_FORCE_LR) {
+        // short-range force over a Verlet list kept fresh by the rebuild rule
+        if (vl_stale(x, R, c) && !vl_rebuild(x, R, c, 0.0)) {
+            if (x.leader()) out->status = BD_ERR_CAPACITY;
+            return;
+        }
+        sr_forces(x, c, c.w.sr_force, c.w.sr_err);
+        if (check_singular(x, R, c, c.w.sr_err, out)) return;
+        const bool add = c.p.force_mode == BD_FORCE_LRSR;
+        for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth())
+            c.s.force[i] = add ? c.s.force[i] + c.w.sr_force[i] : c.w.sr_force[i];
+        x.sync();
+    }
+    if (check_finite(x, R, c, out)) return;
+    // save_state (triangulation.py:158-160) + image counters
+    ph_tri_copy(x, c.s.tri, c.s.tri_backup);
+    if (c.s.image)
+        for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.w.image_bk[i] = c.s.image[i];
+    x.sync();
+
+    double dt_try = c.p.dt;
+    int64_t rollbacks = 0, iters = 0, repairs = 0, flip_passes = 0;
+    bool failed = false;
+    for (;;) {
+        const u64 nc = ph_integrate(x, R, c, dt_try);
+        c.call++;
+        if (nc) ph_apply_crossings(x, c);
+        repairs = 0;
+        flip_passes = 0;
+        int m = maintain(x, R, c, &repairs, &flip_passes);
+        if (m < 0) break;
+        failed = m == 1;
+        if (!failed) {
+            iters = 0;
+            for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) c.s.overlap_flags[i] = 0;
+            int64_t outer;
+            for (outer = 0; outer < c.p.max_overlap_iters; ++outer) {
+                build_edge_incidence(x, c);
+                const int64_t ri = correct_overlaps(x, R, c, EdgePairs{c.s.tri.edge_v, c.s.tri.ne}, true);
+                if (ri < 0) break;
+                iters += ri;
+                if (ri == 0) break;
+                m = maintain(x, R, c, &repairs, &flip_passes);
+                if (m < 0) break;
+                failed = m == 1;
+                if (failed) break;
+            }
+            if (x.ld(&c.w.ctl->status)) break;
+            if (outer == c.p.max_overlap_iters) {
+                set_error(x, c, BD_ERR_NONCONV, 0, 0);
+                x.sync();
+                break;
+            }
+        }
+        if (!failed) break;
+        rollbacks++;
+        if (rollbacks > c.p.max_rollbacks) {
+            set_error(x, c, BD_ERR_STEPFAIL, rollbacks, 0);
+            x.sync();
+            break;
+        }
+        // restore_prev + restore_state, dt halving (dynamics.py:259-261)
+        for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.s.pos[i] = c.s.prev[i];
+        if (c.s.image)
+            for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.s.image[i] = c.w.image_bk[i];
+        ph_tri_copy(x, c.s.tri_backup, c.s.tri);
+        x.sync();
+        dt_try *= 0.5;
+    }
+    // n_overlapping
+    u64* r = R.open();
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) x.add(r, (u64)c.s.overlap_flags[i]);
+    const u64 nov = R.close(r);
+    if (x.leader()) {
+        out->rebuilds = c.s.vl_meta ? c.s.vl_meta[2] - rebuilds0 : 0;
+        out->dt_used = dt_try;
+        out->overlap_iterations = iters;
+        out->flip_passes = flip_passes;
+        out->inversion_repairs = repairs;
+        out->rollbacks = rollbacks;
+        out->n_overlapping = (int64_t)nov;
+        out->status = (int64_t)c.w.ctl->status;
+        out->err_i = (int64_t)c.w.ctl->err_i;
+        out->err_k = (int64_t)c.w.ctl->err_k;
+        *c.s.call = c.call;
+    }
+}
+
+
+// ShortRangeSimulation.step (dynamics.py:326-346): fresh list, short-range
+// force, integrate, overlap rounds over the overlap candidates with list
+// rebuilds whenever motion since the snapshot exceeds skin/2.
+template <class X>
+BD_HD void step_verlet(X& x, Ctx& c, bd_stats_t* out) {
+    Red<X> R(x);
+    if (!driver_enter(x, R, c, out)) return;
+    const int64_t rebuilds0 = c.s.vl_meta[2];
+    const double margin = c.p.sigma + c.p.skin;
+    if (vl_stale(x, R, c) && !vl_rebuild(x, R, c, margin)) {
+        if (x.leader()) out->status = BD_ERR_CAPACITY;
+        return;
+    }
+    sr_forces(x, c, c.s.force, c.s.force_err);
+    if (check_singular(x, R, c, c.s.force_err, out)) return;
+    if (check_finite(x, R, c, out)) return;
+    ph_integrate(x, R, c, c.p.dt);
+    c.call++;
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) c.s.overlap_flags[i] = 0;
+    int64_t iters = 0, round;
+    for (round = 0; round < c.p.max_overlap_iters; ++round) {
+        const SubsetPairs sp{c.s.pair_a, c.s.pair_b, c.w.ov_idx, (int64_t)x.ld((const u64*)&c.s.vl_meta[3])};
+        build_incidence(x, c.p.n, sp, c.w.inc_off, c.w.inc_cur, c.w.inc);
+        const int64_t ri = correct_overlaps(x, R, c, sp, false);
+        if (ri < 0) break;
+        iters += ri;
+        if (!vl_stale(x, R, c)) break;
+        if (!vl_rebuild(x, R, c, margin)) break;
+    }
+    if (!x.ld(&c.w.ctl->status) && round == c.p.max_overlap_iters) {
+        set_error(x, c, BD_ERR_NONCONV, 0, 0);
+        x.sync();
+    }
+    u64* r = R.open();
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) x.add(r, (u64)c.s.overlap_flags[i]);
+    const u64 nov = R.close(r);
+    if (x.leader()) {
+        out->rebuilds = c.s.vl_meta[2] - rebuilds0;
+        out->dt_used = c.p.dt;
+        out->overlap_iterations = iters;
+        out->flip_passes = 0;
+        out->inversion_repairs = 0;
+        out->rollbacks = 0;
+        out->n_overlapping = (int64_t)nov;
+        out->status = (int64_t)c.w.ctl->status;
+        out->err_i = (int64_t)c.w.ctl->err_i;
+        out->err_k = (int64_t)c.w.ctl->err_k;
+        *c.s.call = c.call;
+    }
+}
+
+}  // namespace bd

@@ -12,6 +12,7 @@
 // (and to oracle/bd_oracle.c) on the same inputs and noise.
 #pragma once
 
+#include "bd_allpairs_fast.cuh"
 #include "bd_exec.cuh"
 
 namespace bd {
@@ -21,45 +22,74 @@ enum : uint8_t { ES_NONE = 0, ES_UND = 1, ES_SEL = 2, ES_REM = 3 };
 // workspace carve-up (device pointers)
 struct Ws {
     Ctl* ctl;
-    double* contrib;   // (ne,2) per-edge bounce displacement of the current sweep
+    double* contrib;   // (items,2) per-pair bounce displacement of the current sweep
     uint8_t* estat;    // (ne) flag / selection status
-    uint8_t* eovl;     // (ne) edge overlapping this sweep
+    uint8_t* eovl;     // (items) pair overlapping this sweep
     uint8_t* tinv;     // (nt) triangle inverted
     int8_t* cross8;    // (n,2) crossings mod 256 (all apply_crossings needs)
     int32_t* image_bk; // (n,2)
-    int32_t* inc_off;  // (n+1) CSR offsets of incident edges
+    int32_t* inc_off;  // (n+1) CSR offsets of the overlap neighbour pairs per vertex
     int32_t* inc_cur;  // (n) fill cursors
-    int32_t* inc;      // (2 ne) incident edges, ascending per vertex
-    double* src4;      // (n,4) packed {x, y, alpha, 0} sources of the all-pairs kernel
+    int32_t* inc;      // (2 items) incident pairs, ascending per vertex
+    double* src4;      // all-pairs scratch (packed sources / sorted FAST workspace)
+    // Verlet list (forces.py:67-156)
+    int32_t* cell_id;    // (n)
+    int32_t* cell_start; // (ncells+1)
+    int32_t* cell_cur;   // (ncells)
+    int32_t* corder;     // (n) stable cell order
+    int32_t* pcnt;       // (max(ncells, n)+1) pairs per cell (or per row) -> offsets
+    int32_t* vinc_off;   // (n+1) CSR of Verlet pairs per particle
+    int32_t* vinc_cur;   // (n)
+    int32_t* vinc;       // (2 P)
+    int32_t* ov_idx;     // (P) overlap-candidate subset (ShortRangeSimulation)
+    int64_t* sr_err;     // (n)
+    double* sr_force;    // (n,2) short-range contribution
 };
 
 BD_HD int64_t align_up(int64_t x) { return (x + 255) & ~(int64_t)255; }
 
+BD_HD int64_t ncells_of(const bd_params_t& p) { return p.ncx > 0 ? p.ncx * p.ncx : 0; }
+
 // layout of bd_workspace_bytes(); offsets relative to the workspace base
 struct WsLayout {
-    int64_t ctl, contrib, estat, eovl, tinv, cross8, image_bk, inc_off, inc_cur, inc, src4, total;
+    int64_t ctl, contrib, estat, eovl, tinv, cross8, image_bk, inc_off, inc_cur, inc, src4;
+    int64_t cell_id, cell_start, cell_cur, corder, pcnt, vinc_off, vinc_cur, vinc, ov_idx, sr_err, sr_force, total;
 };
 
-BD_HD WsLayout ws_layout(int64_t n, int64_t ne, int64_t nt) {
+BD_HD WsLayout ws_layout(const bd_params_t& p, int64_t ne, int64_t nt) {
+    const int64_t n = p.n, P = p.pair_capacity > 0 ? p.pair_capacity : 0, nc = ncells_of(p);
+    const int64_t items = ne > P ? ne : P;
     WsLayout l;
     int64_t o = 0;
     l.ctl = o; o = align_up(o + (int64_t)sizeof(Ctl));
-    l.contrib = o; o = align_up(o + 16 * ne);
+    l.contrib = o; o = align_up(o + 16 * items);
     l.estat = o; o = align_up(o + ne);
-    l.eovl = o; o = align_up(o + ne);
+    l.eovl = o; o = align_up(o + items);
     l.tinv = o; o = align_up(o + nt);
     l.cross8 = o; o = align_up(o + 2 * n);
     l.image_bk = o; o = align_up(o + 8 * n);
     l.inc_off = o; o = align_up(o + 4 * (n + 1));
     l.inc_cur = o; o = align_up(o + 4 * n);
-    l.inc = o; o = align_up(o + 8 * ne);
-    l.src4 = o; o = align_up(o + 32 * n);
+    l.inc = o; o = align_up(o + 8 * items);
+    // all-pairs scratch: packed double4 sources (EXACT) or the sorted FAST workspace
+    l.src4 = o; o = align_up(o + (fast_ws_bytes(n) > 32 * n ? fast_ws_bytes(n) : 32 * n));
+    l.cell_id = o; o = align_up(o + (P ? 4 * n : 0));
+    l.cell_start = o; o = align_up(o + (P ? 4 * (nc + 1) : 0));
+    l.cell_cur = o; o = align_up(o + (P ? 4 * nc : 0));
+    l.corder = o; o = align_up(o + (P ? 4 * n : 0));
+    l.pcnt = o; o = align_up(o + (P ? 4 * ((nc > n ? nc : n) + 1) : 0));
+    l.vinc_off = o; o = align_up(o + (P ? 4 * (n + 1) : 0));
+    l.vinc_cur = o; o = align_up(o + (P ? 4 * n : 0));
+    l.vinc = o; o = align_up(o + 8 * P);
+    l.ov_idx = o; o = align_up(o + 4 * P);
+    l.sr_err = o; o = align_up(o + (P ? 8 * n : 0));
+    l.sr_force = o; o = align_up(o + (P ? 16 * n : 0));
     l.total = o;
     return l;
 }
 
-BD_HD Ws ws_carve(void* base, int64_t n, int64_t ne, int64_t nt) {
-    WsLayout l = ws_layout(n, ne, nt);
+BD_HD Ws ws_carve(void* base, const bd_params_t& p, int64_t ne, int64_t nt) {
+    WsLayout l = ws_layout(p, ne, nt);
     char* b = (char*)base;
     Ws w;
     w.ctl = (Ctl*)(b + l.ctl);
@@ -73,6 +103,17 @@ BD_HD Ws ws_carve(void* base, int64_t n, int64_t ne, int64_t nt) {
     w.inc_cur = (int32_t*)(b + l.inc_cur);
     w.inc = (int32_t*)(b + l.inc);
     w.src4 = (double*)(b + l.src4);
+    w.cell_id = (int32_t*)(b + l.cell_id);
+    w.cell_start = (int32_t*)(b + l.cell_start);
+    w.cell_cur = (int32_t*)(b + l.cell_cur);
+    w.corder = (int32_t*)(b + l.corder);
+    w.pcnt = (int32_t*)(b + l.pcnt);
+    w.vinc_off = (int32_t*)(b + l.vinc_off);
+    w.vinc_cur = (int32_t*)(b + l.vinc_cur);
+    w.vinc = (int32_t*)(b + l.vinc);
+    w.ov_idx = (int32_t*)(b + l.ov_idx);
+    w.sr_err = (int64_t*)(b + l.sr_err);
+    w.sr_force = (double*)(b + l.sr_force);
     return w;
 }
 
@@ -405,58 +446,93 @@ BD_HD int maintain(X& x, Red<X>& R, Ctx& c, int64_t* repairs, int64_t* flip_pass
     return 0;
 }
 
-// vertex -> incident edges, ascending edge id (fixes the reference's
-// ascending-pair accumulation order of overlap_pass_kernel)
-template <class X>
-BD_HD void build_incidence(X& x, Ctx& c) {
-    const bd_tri_t& T = c.s.tri;
-    const int64_t n = c.p.n;
-    int32_t* off = c.w.inc_off;
+// Pair sources for the overlap correction / incidence lists: the
+// triangulation edges (dynamics.py:226-229), every Verlet pair, or the
+// Verlet overlap-candidate subset (forces.py:145-149).
+struct EdgePairs {
+    const int32_t* ev;
+    int64_t m;
+    BD_HD int64_t count() const { return m; }
+    BD_HD int64_t a(int64_t e) const { return ev[2 * e]; }
+    BD_HD int64_t b(int64_t e) const { return ev[2 * e + 1]; }
+};
+
+struct ListPairs {
+    const int64_t* pa;
+    const int64_t* pb;
+    int64_t m;
+    BD_HD int64_t count() const { return m; }
+    BD_HD int64_t a(int64_t e) const { return pa[e]; }
+    BD_HD int64_t b(int64_t e) const { return pb[e]; }
+};
+
+struct SubsetPairs {
+    const int64_t* pa;
+    const int64_t* pb;
+    const int32_t* idx;
+    int64_t m;
+    BD_HD int64_t count() const { return m; }
+    BD_HD int64_t a(int64_t e) const { return pa[idx[e]]; }
+    BD_HD int64_t b(int64_t e) const { return pb[idx[e]]; }
+};
+
+// vertex -> incident pairs, ascending pair index (fixes the reference's
+// ascending-pair accumulation order of overlap_pass_kernel / short_range_kernel)
+template <class X, class PS>
+BD_HD void build_incidence(X& x, int64_t n, const PS& ps, int32_t* off, int32_t* cur, int32_t* inc) {
     for (int64_t i = x.tid(); i < n; i += x.nth()) {
         off[i] = 0;
-        c.w.inc_cur[i] = 0;
+        cur[i] = 0;
     }
     x.sync();
-    for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
-        x.fetch_add32(&off[T.edge_v[2 * e]], 1);
-        x.fetch_add32(&off[T.edge_v[2 * e + 1]], 1);
+    const int64_t m = ps.count();
+    for (int64_t e = x.tid(); e < m; e += x.nth()) {
+        x.fetch_add32(&off[ps.a(e)], 1);
+        x.fetch_add32(&off[ps.b(e)], 1);
     }
     x.sync();
     x.exclusive_scan(off, n);
-    for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
-        const int64_t a = T.edge_v[2 * e], b = T.edge_v[2 * e + 1];
-        c.w.inc[off[a] + x.fetch_add32(&c.w.inc_cur[a], 1)] = (int32_t)e;
-        c.w.inc[off[b] + x.fetch_add32(&c.w.inc_cur[b], 1)] = (int32_t)e;
+    for (int64_t e = x.tid(); e < m; e += x.nth()) {
+        const int64_t a = ps.a(e), b = ps.b(e);
+        inc[off[a] + x.fetch_add32(&cur[a], 1)] = (int32_t)e;
+        inc[off[b] + x.fetch_add32(&cur[b], 1)] = (int32_t)e;
     }
     x.sync();
     for (int64_t i = x.tid(); i < n; i += x.nth()) {
-        int32_t* L = c.w.inc + off[i];
-        const int32_t m = off[i + 1] - off[i];
-        for (int32_t j = 1; j < m; ++j) {
-            const int32_t v = L[j];
-            int32_t k = j - 1;
-            while (k >= 0 && L[k] > v) {
-                L[k + 1] = L[k];
-                --k;
+        int32_t* Lst = inc + off[i];
+        const int32_t k = off[i + 1] - off[i];
+        for (int32_t j = 1; j < k; ++j) {
+            const int32_t v = Lst[j];
+            int32_t q = j - 1;
+            while (q >= 0 && Lst[q] > v) {
+                Lst[q + 1] = Lst[q];
+                --q;
             }
-            L[k + 1] = v;
+            Lst[q + 1] = v;
         }
     }
     x.sync();
 }
 
-// correct_overlaps (dynamics.py:97-133) over the triangulation edges; returns
-// sweeps, or -1 on non-convergence
 template <class X>
-BD_HD int64_t correct_overlaps_tri(X& x, Red<X>& R, Ctx& c) {
-    const bd_tri_t& T = c.s.tri;
+BD_HD void build_edge_incidence(X& x, Ctx& c) {
+    const EdgePairs ps{c.s.tri.edge_v, c.s.tri.ne};
+    build_incidence(x, c.p.n, ps, c.w.inc_off, c.w.inc_cur, c.w.inc);
+}
+
+// correct_overlaps (dynamics.py:97-133) over a fixed pair set with its
+// incidence lists in w.inc_off / w.inc; `tri` -> crossings feed
+// apply_crossings (dynamics.py:127-129).  Returns sweeps, -1 on non-convergence.
+template <class X, class PS>
+BD_HD int64_t correct_overlaps(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri) {
     const double L = c.p.L, sigma = c.p.sigma, thresh = sigma * (1.0 - 1e-9), cap = c.p.cap;
     double* pos = c.s.pos;
+    const int64_t m = ps.count();
     int64_t iterations = 0;
     for (int64_t it = 0; it < c.p.max_overlap_iters; ++it) {
         u64* r = R.open();
-        for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
-            const int64_t a = T.edge_v[2 * e], b = T.edge_v[2 * e + 1];
+        for (int64_t e = x.tid(); e < m; e += x.nth()) {
+            const int64_t a = ps.a(e), b = ps.b(e);
             const double dx = mi_exact(pos[2 * b] - pos[2 * a], c.p), dy = mi_exact(pos[2 * b + 1] - pos[2 * a + 1], c.p);
             const double rr = sqrt(dx * dx + dy * dy);
             const bool ov = !(rr >= thresh || rr == 0.0);
@@ -481,7 +557,7 @@ BD_HD int64_t correct_overlaps_tri(X& x, Red<X>& R, Ctx& c) {
                 if (!c.w.eovl[e]) continue;
                 hit = true;
                 const double cx = c.w.contrib[2 * e], cy = c.w.contrib[2 * e + 1];
-                if (T.edge_v[2 * e] == i) {
+                if (ps.a(e) == i) {
                     dx -= cx;
                     dy -= cy;
                 } else {
@@ -511,140 +587,11 @@ BD_HD int64_t correct_overlaps_tri(X& x, Red<X>& R, Ctx& c) {
             }
             x.add(rc, (u64)crossed);
         }
-        if (R.close(rc)) ph_apply_crossings(x, c);
+        if (R.close(rc) && tri) ph_apply_crossings(x, c);
     }
     set_error(x, c, BD_ERR_NONCONV, 0, 0);
     x.sync();
     return -1;
-}
-
-// LongRangeSimulation.step after the force evaluation (dynamics.py:196-274).
-// The forces of this step are already in s.force (computed by the all-pairs
-// kernel / Verlet force on the pre-move positions).
-template <class X>
-BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
-    Red<X> R(x);
-    if (x.leader())
-        for (int k = 0; k < 8; ++k) c.w.ctl->red[k] = 0;
-    x.sync();
-    if (x.ld(&c.w.ctl->status)) {  // an earlier step failed: this one does not run
-        if (x.leader()) out->status = -1;
-        return;
-    }
-    // singularity sentinels of the force kernels (forces.py:54-58: first i, k = err[i]-1)
-    {
-        u64* r = R.open();
-        if (x.leader()) c.w.ctl->scratch[1] = ~0ull;
-        x.sync();
-        for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
-            const bool bad = c.s.force_err[i] != 0;
-            if (bad) x.umin(&c.w.ctl->scratch[1], (u64)i);
-            x.add(r, (u64)bad);
-        }
-        if (R.close(r)) {
-            if (x.leader()) {
-                const int64_t i = (int64_t)c.w.ctl->scratch[1];
-                c.w.ctl->status = BD_ERR_SINGULAR;
-                c.w.ctl->err_i = (u64)i;
-                c.w.ctl->err_k = (u64)(c.s.force_err[i] - 1);
-                out->status = BD_ERR_SINGULAR;
-                out->err_i = i;
-                out->err_k = c.s.force_err[i] - 1;
-            }
-            return;
-        }
-    }
-    // finite-force check (integrate, dynamics.py:84-86)
-    {
-        u64* r = R.open();
-        if (x.leader()) c.w.ctl->scratch[0] = ~0ull;
-        x.sync();
-        for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
-            const bool bad = !(isfinite(c.s.force[2 * i]) && isfinite(c.s.force[2 * i + 1]));
-            if (bad) x.umin(&c.w.ctl->scratch[0], (u64)i);
-            x.add(r, (u64)bad);
-        }
-        if (R.close(r)) {
-            if (x.leader()) {
-                c.w.ctl->status = BD_ERR_STEPFAIL;
-                c.w.ctl->err_i = c.w.ctl->scratch[0];
-                out->status = BD_ERR_STEPFAIL;
-                out->err_i = (int64_t)c.w.ctl->scratch[0];
-            }
-            return;
-        }
-    }
-    // save_state (triangulation.py:158-160) + image counters
-    ph_tri_copy(x, c.s.tri, c.s.tri_backup);
-    if (c.s.image)
-        for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.w.image_bk[i] = c.s.image[i];
-    x.sync();
-
-    double dt_try = c.p.dt;
-    int64_t rollbacks = 0, iters = 0, repairs = 0, flip_passes = 0;
-    bool failed = false;
-    for (;;) {
-        const u64 nc = ph_integrate(x, R, c, dt_try);
-        c.call++;
-        if (nc) ph_apply_crossings(x, c);
-        repairs = 0;
-        flip_passes = 0;
-        int m = maintain(x, R, c, &repairs, &flip_passes);
-        if (m < 0) break;
-        failed = m == 1;
-        if (!failed) {
-            iters = 0;
-            for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) c.s.overlap_flags[i] = 0;
-            int64_t outer;
-            for (outer = 0; outer < c.p.max_overlap_iters; ++outer) {
-                build_incidence(x, c);
-                const int64_t ri = correct_overlaps_tri(x, R, c);
-                if (ri < 0) break;
-                iters += ri;
-                if (ri == 0) break;
-                m = maintain(x, R, c, &repairs, &flip_passes);
-                if (m < 0) break;
-                failed = m == 1;
-                if (failed) break;
-            }
-            if (x.ld(&c.w.ctl->status)) break;
-            if (outer == c.p.max_overlap_iters) {
-                set_error(x, c, BD_ERR_NONCONV, 0, 0);
-                x.sync();
-                break;
-            }
-        }
-        if (!failed) break;
-        rollbacks++;
-        if (rollbacks > c.p.max_rollbacks) {
-            set_error(x, c, BD_ERR_STEPFAIL, rollbacks, 0);
-            x.sync();
-            break;
-        }
-        // restore_prev + restore_state, dt halving (dynamics.py:259-261)
-        for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.s.pos[i] = c.s.prev[i];
-        if (c.s.image)
-            for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.s.image[i] = c.w.image_bk[i];
-        ph_tri_copy(x, c.s.tri_backup, c.s.tri);
-        x.sync();
-        dt_try *= 0.5;
-    }
-    // n_overlapping
-    u64* r = R.open();
-    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) x.add(r, (u64)c.s.overlap_flags[i]);
-    const u64 nov = R.close(r);
-    if (x.leader()) {
-        out->dt_used = dt_try;
-        out->overlap_iterations = iters;
-        out->flip_passes = flip_passes;
-        out->inversion_repairs = repairs;
-        out->rollbacks = rollbacks;
-        out->n_overlapping = (int64_t)nov;
-        out->status = (int64_t)c.w.ctl->status;
-        out->err_i = (int64_t)c.w.ctl->err_i;
-        out->err_k = (int64_t)c.w.ctl->err_k;
-        *c.s.call = c.call;
-    }
 }
 
 }  // namespace bd

@@ -1,0 +1,240 @@
+// bd_verlet.cuh -- short-range force path on the device: Verlet list build
+// (cell grid + ordered pair emission), staleness test, short-range forces,
+// overlap-candidate subset.  Same uniform-phase style as bd_step.cuh.
+//
+// Reference: build_cell_grid forces.py:81-99, _kernels.cell_pairs
+// _kernels.py:141-236, build_verlet forces.py:120-150, verlet_needs_rebuild
+// forces.py:153-156 (max_sq_displacement _kernels.py:128-138),
+// short_range_kernel _kernels.py:62-91.
+//
+// Bit-exactness: the pair list has exactly the reference's order (cells
+// ascending; same cell ia < ib in stable cell order; half-neighbourhood
+// offsets (1,0), (-1,1), (0,1), (1,1); a in c x b in d), produced by one
+// thread per cell in two passes (count, fill) around a scan.  Short-range
+// forces are gathered per particle over its incident pairs in ascending pair
+// index, reproducing the reference's sequential += / -= order.
+#pragma once
+
+#include "bd_step.cuh"
+
+namespace bd {
+
+// half-neighbourhood offsets (1,0), (-1,1), (0,1), (1,1) (_kernels.py:159-167)
+BD_HD int off_x(int k) { return k == 0 ? 1 : (k == 1 ? -1 : (k == 2 ? 0 : 1)); }
+BD_HD int off_y(int k) { return k == 0 ? 0 : 1; }
+
+// pairs of one cell in the reference's nested-loop order; FILL writes them
+template <bool FILL>
+BD_HD int64_t cell_pairs_of(const Ctx& c, int64_t cell, int64_t k0) {
+    const int64_t ncx = c.p.ncx;
+    const int64_t cx = cell % ncx, cy = cell / ncx;
+    const int32_t a0 = c.w.cell_start[cell], a1 = c.w.cell_start[cell + 1];
+    const double rl2 = c.p.r_list * c.p.r_list;
+    const double* pos = c.s.pos;
+    int64_t k = k0;
+    for (int32_t ia = a0; ia < a1; ++ia) {
+        const int64_t a = c.w.corder[ia];
+        for (int32_t ib = ia + 1; ib < a1; ++ib) {
+            const int64_t b = c.w.corder[ib];
+            const double dx = mi_exact(pos[2 * a] - pos[2 * b], c.p), dy = mi_exact(pos[2 * a + 1] - pos[2 * b + 1], c.p);
+            if (dx * dx + dy * dy <= rl2) {
+                if (FILL) {
+                    c.s.pair_a[k] = a;
+                    c.s.pair_b[k] = b;
+                }
+                ++k;
+            }
+        }
+    }
+    for (int off = 0; off < 4; ++off) {
+        const int64_t d = ((cx + off_x(off) + ncx) % ncx) + ((cy + off_y(off)) % ncx) * ncx;
+        const int32_t b0 = c.w.cell_start[d], b1 = c.w.cell_start[d + 1];
+        for (int32_t ia = a0; ia < a1; ++ia) {
+            const int64_t a = c.w.corder[ia];
+            for (int32_t ib = b0; ib < b1; ++ib) {
+                const int64_t b = c.w.corder[ib];
+                const double dx = mi_exact(pos[2 * a] - pos[2 * b], c.p),
+                             dy = mi_exact(pos[2 * a + 1] - pos[2 * b + 1], c.p);
+                if (dx * dx + dy * dy <= rl2) {
+                    if (FILL) {
+                        c.s.pair_a[k] = a;
+                        c.s.pair_b[k] = b;
+                    }
+                    ++k;
+                }
+            }
+        }
+    }
+    return k - k0;
+}
+
+// one row a of np.triu_indices(n, 1) within r_list (forces.py:136-141, no grid)
+template <bool FILL>
+BD_HD int64_t brute_pairs_of(const Ctx& c, int64_t a, int64_t k0) {
+    const double rl2 = c.p.r_list * c.p.r_list;
+    const double* pos = c.s.pos;
+    int64_t k = k0;
+    for (int64_t b = a + 1; b < c.p.n; ++b) {
+        const double dx = mi_exact(pos[2 * b] - pos[2 * a], c.p), dy = mi_exact(pos[2 * b + 1] - pos[2 * a + 1], c.p);
+        if (dx * dx + dy * dy <= rl2) {
+            if (FILL) {
+                c.s.pair_a[k] = a;
+                c.s.pair_b[k] = b;
+            }
+            ++k;
+        }
+    }
+    return k - k0;
+}
+
+// verlet_needs_rebuild: never built, or max |mi(pos - snap)|^2 > (skin/2)^2
+template <class X>
+BD_HD bool vl_stale(X& x, Red<X>& R, Ctx& c) {
+    if (x.ld((const u64*)&c.s.vl_meta[1]) == 0) return true;
+    u64* r = R.open();
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
+        const double dx = mi_exact(c.s.pos[2 * i] - c.s.vl_snap[2 * i], c.p);
+        const double dy = mi_exact(c.s.pos[2 * i + 1] - c.s.vl_snap[2 * i + 1], c.p);
+        const double d2 = dx * dx + dy * dy;
+        x.umax(r, double_to_bits(d2));
+    }
+    const double worst = bits_to_double(R.close(r));
+    const double h = c.p.skin / 2.0;
+    return worst > h * h;
+}
+
+// build_cell_grid + cell_pairs + snapshot (+ overlap subset within `margin`
+// when margin > 0, + the per-particle pair incidence for the force gather).
+// Returns false on a capacity overflow (status BD_ERR_CAPACITY).
+template <class X>
+BD_HD bool vl_rebuild(X& x, Red<X>& R, Ctx& c, double margin) {
+    const int64_t n = c.p.n, ncx = c.p.ncx;
+    int32_t* cnt = c.w.pcnt;
+    int64_t rows;
+    if (ncx >= 3) {
+        const int64_t nc = ncx * ncx;
+        const double edge = c.p.L / (double)ncx;
+        for (int64_t k = x.tid(); k < nc; k += x.nth()) {
+            c.w.cell_start[k] = 0;
+            c.w.cell_cur[k] = 0;
+        }
+        x.sync();
+        for (int64_t i = x.tid(); i < n; i += x.nth()) {
+            int64_t ix = (int64_t)floor(c.s.pos[2 * i] / edge), iy = (int64_t)floor(c.s.pos[2 * i + 1] / edge);
+            ix = ix < 0 ? 0 : (ix > ncx - 1 ? ncx - 1 : ix);
+            iy = iy < 0 ? 0 : (iy > ncx - 1 ? ncx - 1 : iy);
+            const int32_t cid = (int32_t)(ix + iy * ncx);
+            c.w.cell_id[i] = cid;
+            x.fetch_add32(&c.w.cell_start[cid], 1);
+        }
+        x.sync();
+        x.exclusive_scan(c.w.cell_start, nc);
+        for (int64_t i = x.tid(); i < n; i += x.nth()) {
+            const int32_t cid = c.w.cell_id[i];
+            c.w.corder[c.w.cell_start[cid] + x.fetch_add32(&c.w.cell_cur[cid], 1)] = (int32_t)i;
+        }
+        x.sync();
+        // stable argsort: ascending particle index inside each cell
+        for (int64_t k = x.tid(); k < nc; k += x.nth()) {
+            int32_t* a = c.w.corder + c.w.cell_start[k];
+            const int32_t m = c.w.cell_start[k + 1] - c.w.cell_start[k];
+            for (int32_t j = 1; j < m; ++j) {
+                const int32_t v = a[j];
+                int32_t q = j - 1;
+                while (q >= 0 && a[q] > v) {
+                    a[q + 1] = a[q];
+                    --q;
+                }
+                a[q + 1] = v;
+            }
+        }
+        x.sync();
+        for (int64_t k = x.tid(); k < nc; k += x.nth()) cnt[k] = (int32_t)cell_pairs_of<false>(c, k, 0);
+        rows = nc;
+    } else {
+        for (int64_t a = x.tid(); a < n; a += x.nth()) cnt[a] = (int32_t)brute_pairs_of<false>(c, a, 0);
+        rows = n;
+    }
+    x.sync();
+    x.exclusive_scan(cnt, rows);
+    const int64_t total = cnt[rows];
+    if (total > c.p.pair_capacity) {
+        set_error(x, c, BD_ERR_CAPACITY, total, c.p.pair_capacity);
+        x.sync();
+        return false;
+    }
+    if (ncx >= 3)
+        for (int64_t k = x.tid(); k < rows; k += x.nth()) cell_pairs_of<true>(c, k, cnt[k]);
+    else
+        for (int64_t a = x.tid(); a < rows; a += x.nth()) brute_pairs_of<true>(c, a, cnt[a]);
+    for (int64_t i = x.tid(); i < 2 * n; i += x.nth()) c.s.vl_snap[i] = c.s.pos[i];
+    x.sync();
+    // incidence of the Verlet pairs (ascending pair index per particle)
+    const ListPairs lp{c.s.pair_a, c.s.pair_b, total};
+    build_incidence(x, n, lp, c.w.vinc_off, c.w.vinc_cur, c.w.vinc);
+    int64_t nov = 0;
+    if (margin > 0.0) {
+        // overlap candidates: pairs within margin at build time, order kept (forces.py:145-149)
+        int32_t* flag = (int32_t*)c.w.contrib;  // scratch (>= 4 (P+1) bytes)
+        const double m2 = margin * margin;
+        for (int64_t e = x.tid(); e < total; e += x.nth()) {
+            const int64_t a = c.s.pair_a[e], b = c.s.pair_b[e];
+            const double dx = mi_exact(c.s.pos[2 * b] - c.s.pos[2 * a], c.p);
+            const double dy = mi_exact(c.s.pos[2 * b + 1] - c.s.pos[2 * a + 1], c.p);
+            flag[e] = (dx * dx + dy * dy) <= m2 ? 1 : 0;
+        }
+        x.sync();
+        x.exclusive_scan(flag, total);
+        nov = flag[total];
+        for (int64_t e = x.tid(); e < total; e += x.nth())
+            if (flag[e + 1] != flag[e]) c.w.ov_idx[flag[e]] = (int32_t)e;
+        x.sync();
+    }
+    if (x.leader()) {
+        c.s.vl_meta[0] = total;
+        c.s.vl_meta[1] = 1;
+        c.s.vl_meta[2] += 1;
+        c.s.vl_meta[3] = nov;
+    }
+    x.sync();
+    return true;
+}
+
+// short_range_kernel (_kernels.py:62-91) gathered per particle: out[i], err[i]
+template <class X>
+BD_HD void sr_forces(X& x, Ctx& c, double* out, int64_t* err) {
+    const double rc2 = c.p.r_cut * c.p.r_cut;
+    const double* pos = c.s.pos;
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
+        double fx = 0.0, fy = 0.0;
+        int64_t e = 0;
+        const int32_t j0 = c.w.vinc_off[i], j1 = c.w.vinc_off[i + 1];
+        for (int32_t j = j0; j < j1; ++j) {
+            const int64_t q = c.w.vinc[j];
+            const int64_t a = c.s.pair_a[q], b = c.s.pair_b[q];
+            const double dx = mi_exact(pos[2 * a] - pos[2 * b], c.p), dy = mi_exact(pos[2 * a + 1] - pos[2 * b + 1], c.p);
+            const double r2 = dx * dx + dy * dy;
+            if (r2 > rc2) continue;
+            if (r2 == 0.0) {
+                if (a == i) e = b + 1;
+                continue;
+            }
+            const double inv7 = 1.0 / (r2 * r2 * r2 * sqrt(r2));
+            if (a == i) {
+                const double wa = c.s.mu[a] * c.s.alpha[b] * inv7;
+                fx += wa * dx;
+                fy += wa * dy;
+            } else {
+                const double wb = c.s.mu[b] * c.s.alpha[a] * inv7;
+                fx -= wb * dx;
+                fy -= wb * dy;
+            }
+        }
+        out[2 * i] = fx;
+        out[2 * i + 1] = fy;
+        err[i] = e;
+    }
+    x.sync();
+}
+
+}  // namespace bd

@@ -1,44 +1,45 @@
 """Step loops on the GPU, with the reference's API.
 
-LongRangeSimulation mirrors brownsim.dynamics.LongRangeSimulation
-(dynamics.py:177-274): constructor (sys, params, rng, tri=None,
-debug_scan=False, collect_flags=False), step() -> StepStats, run(steps,
-on_step) -> list[StepStats], state read-out via .sys / .tri /
-.last_overlap_flags / .step_index.  Each step is two launches on the current
-CUDA stream: the all-pairs force kernel and ONE persistent cooperative
-kernel that runs integrate, the pass-through check, inversion repair,
-Delaunay flips, overlap correction, the joint fixed point and the rollback
-loop entirely on the device (csrc/bd_step.cuh).  The host reads back only
-the StepStats counters.
+LongRangeSimulation and ShortRangeSimulation mirror brownsim.dynamics
+(dynamics.py:177-346): constructors (sys, params, rng, ...), step() ->
+StepStats, run(steps, on_step) -> list[StepStats], state read-out via .sys,
+.tri, .last_overlap_flags, .step_index, .rebuilds.
 
-Extra keyword arguments (not in the reference):
+A long-range step is two launches on the current CUDA stream: the all-pairs
+force kernel and ONE persistent cooperative kernel that runs integrate, the
+pass-through check, inversion repair, Delaunay flips, overlap correction,
+the joint fixed point and the rollback loop entirely on the device
+(csrc/bd_drivers.cuh).  A short-range step is one persistent kernel (Verlet
+list maintenance, short-range force, integrate, overlap rounds).  The host
+reads back only the StepStats counters (16 words per step, once per run()).
+
+Extra keyword arguments of LongRangeSimulation (not in the reference):
   force        "long-range" (default), "short-range" or "long+short" -- the
-               composite force models of SURVEY.md §0 (Verlet-list short
-               range, r_cutoff from params), with the triangulation as the
-               overlap neighbour provider in every case;
-  precision    "exact" (bit-identical to the reference) or "fast" (FMA +
-               rsqrt all-pairs, |dF|/|F| ~1e-12);
-  skin         Verlet skin for the short-range force (default sigma/2).
+               composite force models of SURVEY.md §0 (Verlet-list short range
+               with params.r_cutoff); the triangulation stays the overlap
+               neighbour provider in every case;
+  precision    "exact" (bit-identical to the reference) or "fast" (sorted,
+               FMA + rsqrt all-pairs; |dF|/|F| ~1e-13);
+  skin         Verlet skin for the short-range force (default sigma / 2).
 """
 
 from __future__ import annotations
 
 import ctypes
-import time
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _abi
 from ._lib import check, lib, require_cuda
-from .core import (BrownsimError, CounterRng, NonConvergenceError, ParticleSystem, SimParams,
-                   SingularityError, StepFailure)
+from .core import (BrownsimError, CounterRng, NonConvergenceError, ParticleSystem, SimParams, SingularityError,
+                   StepFailure)
+from .forces import verlet_pair_capacity
 from .triangulation import TRI_KEYS, PeriodicTriangulation
 
 RESOLVE_FRAC = 1.0 - 1e-9  # dynamics.py:39
 
-FORCE_MODES = {"long-range": _abi.BD_FORCE_LR, "short-range": _abi.BD_FORCE_SR,
-               "long+short": _abi.BD_FORCE_LRSR}
+FORCE_MODES = {"long-range": _abi.BD_FORCE_LR, "short-range": _abi.BD_FORCE_SR, "long+short": _abi.BD_FORCE_LRSR}
 PRECISIONS = {"exact": _abi.BD_LR_EXACT, "fast": _abi.BD_LR_FAST}
 
 
@@ -61,7 +62,7 @@ class StepStats:
 
 
 class MissedOverlapError(BrownsimError):
-    """Debug scan found an overlapping pair the neighbour provider missed."""
+    """Debug scan found an overlapping pair the neighbour provider missed (dynamics.py:69-70)."""
 
 
 def _tri_struct(tensors: dict, nv: int) -> _abi.BdTri:
@@ -75,7 +76,7 @@ def _stream():
 
 
 def make_params(params: SimParams, box_length: float, seed: int, stream: int, force_mode: int = 0,
-                precision: int = 0, skin: float | None = None) -> _abi.BdParams:
+                precision: int = 0, skin: float | None = None, pairs: bool = False) -> _abi.BdParams:
     p = _abi.BdParams()
     p.n = params.n
     p.L = float(box_length)
@@ -87,7 +88,8 @@ def make_params(params: SimParams, box_length: float, seed: int, stream: int, fo
     p.max_overlap_iters, p.max_rollbacks = int(params.max_overlap_iters), int(params.max_rollbacks)
     p.seed, p.stream = int(seed) & ((1 << 64) - 1), int(stream) & ((1 << 64) - 1)
     p.force_mode, p.lr_precision = int(force_mode), int(precision)
-    lib().bd_prepare_params(ctypes.byref(p))
+    lib().bd_prepare_params(ctypes.byref(p))  # mi breakpoints, r_list, ncx
+    p.pair_capacity = verlet_pair_capacity(params.n, box_length, p.r_list, params.sigma) if pairs else 0
     return p
 
 
@@ -103,9 +105,14 @@ class _Engine:
         self.overlap_flags = torch.zeros(n, dtype=torch.uint8, device=dev)
         self.call_t = torch.tensor([call], dtype=torch.int64, device=dev)
         self.stats_t = torch.zeros(_abi.STATS_WORDS, dtype=torch.int64, device=dev)
+        cap = int(bparams.pair_capacity)
+        self.pair_a = torch.zeros(max(cap, 1), dtype=torch.int64, device=dev)
+        self.pair_b = torch.zeros(max(cap, 1), dtype=torch.int64, device=dev)
+        self.vl_snap = torch.zeros((n, 2), dtype=torch.float64, device=dev)
+        self.vl_meta = torch.zeros(8, dtype=torch.int64, device=dev)
         ne = tri.n_edges if tri is not None else 0
         nt = tri.n_triangles if tri is not None else 0
-        wb = lib().bd_workspace_bytes(n, ne, nt, int(bparams.pair_capacity))
+        wb = lib().bd_workspace_bytes(ctypes.byref(bparams), ne, nt)
         self.work = torch.zeros(wb // 8 + 64, dtype=torch.int64, device=dev)
         s = _abi.BdState()
         s.pos, s.prev, s.force = sys.positions_t.data_ptr(), sys.positions_prev_t.data_ptr(), sys.forces_t.data_ptr()
@@ -118,6 +125,8 @@ class _Engine:
             s.tri_backup = _tri_struct(tri.backup_tensors(), n)
         s.call = self.call_t.data_ptr()
         s.stats = self.stats_t.data_ptr()
+        s.pair_a, s.pair_b = self.pair_a.data_ptr(), self.pair_b.data_ptr()
+        s.vl_snap, s.vl_meta = self.vl_snap.data_ptr(), self.vl_meta.data_ptr()
         s.work = self.work.data_ptr()
         s.work_bytes = self.work.numel() * 8
         self.s = s
@@ -139,15 +148,21 @@ def _raise_for(st: dict, step_index: int):
                           f"(particle/rollbacks {st['err_i']})")
     if code == _abi.BD_ERR_FLIP:
         raise BrownsimError(f"step {step_index}: edge {st['err_i']} not flippable")
+    if code == _abi.BD_ERR_CAPACITY:
+        raise BrownsimError(f"step {step_index}: Verlet list of {st['err_i']} pairs exceeds capacity {st['err_k']}")
     raise BrownsimError(f"step {step_index}: device status {code}")
 
 
 def _decode_stats(words: np.ndarray) -> dict:
     raw = _abi.BdStats.from_buffer_copy(np.ascontiguousarray(words, dtype=np.int64).tobytes())
-    return {k: (getattr(raw, k) if k != "reserved" else None) for k, _ in _abi.BdStats._fields_}
+    return {k: getattr(raw, k) for k, _ in _abi.BdStats._fields_ if k != "reserved"}
 
 
 class _SimulationBase:
+    """Shared run loop (dynamics.py:149-174); subclasses provide the launches."""
+
+    _two_phase = False  # force kernel + driver kernel (timed separately)
+
     def __init__(self, sys: ParticleSystem, params: SimParams, rng, debug_scan=False, collect_flags=False):
         self.sys = sys
         self.params = params
@@ -160,8 +175,74 @@ class _SimulationBase:
     def last_overlap_flags(self) -> np.ndarray:
         return self._eng.overlap_flags.cpu().numpy().astype(bool)
 
-    def _sync_rng(self):
+    @property
+    def rebuilds(self) -> int:
+        return int(self._eng.vl_meta[2].item())
+
+    def _refresh_params(self):
+        # the reference lets callers mutate sim.params between steps (e.g. dt)
+        p, b = self.params, self.bparams
+        b.dt, b.diffusion = float(p.dt), float(p.diffusion)
+        b.max_overlap_iters, b.max_rollbacks = int(p.max_overlap_iters), int(p.max_rollbacks)
+        b.cap, b.clamp = float(p.displacement_cap), float(p.noise_clamp)
+
+    def step(self) -> StepStats:
+        return self.run(1)[0]
+
+    def run(self, steps: int, on_step=None) -> list:
+        """`steps` steps; without on_step / debug_scan / collect_flags they are
+        queued back to back with a single host synchronisation at the end."""
+        self._refresh_params()
+        if steps <= 0:
+            return []
+        self._eng.clear_status()
+        if on_step is None and not self.debug_scan and not self.collect_flags:
+            return self._run_batch(steps)
+        out = []
+        for _ in range(steps):
+            out.extend(self._run_batch(1))
+            if self.debug_scan:
+                from .validation import debug_overlap_scan
+                debug_overlap_scan(self.sys, self.params)
+            if on_step is not None:
+                on_step(self, out[-1])
+        return out
+
+    def _launch_force(self):
+        pass
+
+    def _launch_driver(self, stats_ptr: int):
+        raise NotImplementedError
+
+    def _run_batch(self, steps: int) -> list:
+        import torch
+        stats = torch.zeros((steps, _abi.STATS_WORDS), dtype=torch.int64, device=self.sys.device)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps + 1)]
+        evs[0].record()
+        for j in range(steps):
+            self._launch_force()
+            evs[2 * j + 1].record()
+            self._launch_driver(stats[j].data_ptr())
+            evs[2 * j + 2].record()
+        host = stats.cpu().numpy()
         self.rng.call = int(self._eng.call_t.item())
+        res = []
+        for j in range(steps):
+            st = _decode_stats(host[j])
+            if st["status"] == -1:
+                break
+            force_ms = evs[2 * j].elapsed_time(evs[2 * j + 1])
+            drv_ms = evs[2 * j + 1].elapsed_time(evs[2 * j + 2])
+            _raise_for(st, self.step_index)
+            flags = self.last_overlap_flags.copy() if self.collect_flags else None
+            res.append(StepStats(step=self.step_index, dt_used=st["dt_used"],
+                                 overlap_iterations=st["overlap_iterations"], flip_passes=st["flip_passes"],
+                                 inversion_repairs=st["inversion_repairs"], rollbacks=st["rollbacks"],
+                                 n_overlapping=st["n_overlapping"],
+                                 force_ms=force_ms if self._two_phase else 0.0,
+                                 maintain_ms=drv_ms, overlap_ms=0.0, step_ms=force_ms + drv_ms, overlap_flags=flags))
+            self.step_index += 1
+        return res
 
 
 def device_restore_delaunay(tri: PeriodicTriangulation, positions, box, tol=1e-12) -> int:
@@ -193,7 +274,10 @@ def device_restore_delaunay(tri: PeriodicTriangulation, positions, box, tol=1e-1
 
 class LongRangeSimulation(_SimulationBase):
     """All-pairs forces with a continuously maintained triangulation
-    (dynamics.py:177-274), every phase on the GPU."""
+    (dynamics.py:177-274), every phase on the GPU; optionally the composite
+    short-range / long+short force models (see module docstring)."""
+
+    _two_phase = True
 
     def __init__(self, sys: ParticleSystem, params: SimParams, rng=None, tri: PeriodicTriangulation | None = None,
                  debug_scan: bool = False, collect_flags: bool = False, force: str = "long-range",
@@ -211,75 +295,51 @@ class LongRangeSimulation(_SimulationBase):
             raise BrownsimError(f"unknown precision {precision!r}; have {sorted(PRECISIONS)}")
         self.force_model = force
         self.precision = precision
+        self.skin = 0.5 * params.sigma if skin is None else float(skin)
         self.bparams = make_params(params, sys.box.length, self.rng.seed, self.rng.stream, FORCE_MODES[force],
-                                   PRECISIONS[precision], skin)
+                                   PRECISIONS[precision], skin, pairs=force != "long-range")
         self._eng = _Engine(sys, tri, self.bparams, self.rng.call)
         self._eng.clear_status()
 
-    def _refresh_params(self):
-        # the reference lets tests mutate sim.params between steps (e.g. dt)
-        p = self.params
-        b = self.bparams
-        b.dt, b.diffusion = float(p.dt), float(p.diffusion)
-        b.max_overlap_iters, b.max_rollbacks = int(p.max_overlap_iters), int(p.max_rollbacks)
-        b.cap, b.clamp = float(p.displacement_cap), float(p.noise_clamp)
+    def _launch_force(self):
+        check(lib().bd_force(ctypes.byref(self._eng.s), ctypes.byref(self.bparams), _stream()), "bd_force")
 
-    def _launch_step(self, stats_ptr: int):
-        L = lib()
-        check(L.bd_force(ctypes.byref(self._eng.s), ctypes.byref(self.bparams), _stream()), "bd_force")
-        check(L.bd_maintain_tri(ctypes.byref(self._eng.s), ctypes.byref(self.bparams), ctypes.c_void_p(stats_ptr),
-                                _stream()), "bd_maintain_tri")
+    def _launch_driver(self, stats_ptr: int):
+        check(lib().bd_maintain_tri(ctypes.byref(self._eng.s), ctypes.byref(self.bparams),
+                                    ctypes.c_void_p(stats_ptr), _stream()), "bd_maintain_tri")
 
-    def step(self) -> StepStats:
-        return self.run(1)[0]
 
-    def run(self, steps: int, on_step=None) -> list:
-        """`steps` steps; without on_step/debug_scan they are queued back to
-        back with a single host synchronisation at the end."""
-        import torch
-        self._refresh_params()
-        if steps <= 0:
-            return []
-        per_step_host = on_step is not None or self.debug_scan or self.collect_flags
-        out = []
-        if per_step_host:
-            for _ in range(steps):
-                out.extend(self._run_batch(1))
-                if self.debug_scan:
-                    from .validation import debug_overlap_scan
-                    debug_overlap_scan(self.sys, self.params)
-                if on_step is not None:
-                    on_step(self, out[-1])
-            return out
-        return self._run_batch(steps)
+class ShortRangeSimulation(_SimulationBase):
+    """Cutoff forces over Verlet lists; no triangulation (dynamics.py:307-346).
 
-    def _run_batch(self, steps: int) -> list:
-        import torch
-        stats = torch.zeros((steps, _abi.STATS_WORDS), dtype=torch.int64, device=self.sys.device)
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps + 1)]
-        evs[0].record()
-        for j in range(steps):
-            L = lib()
-            check(L.bd_force(ctypes.byref(self._eng.s), ctypes.byref(self.bparams), _stream()), "bd_force")
-            evs[2 * j + 1].record()
-            check(L.bd_maintain_tri(ctypes.byref(self._eng.s), ctypes.byref(self.bparams),
-                                    ctypes.c_void_p(stats[j].data_ptr()), _stream()), "bd_maintain_tri")
-            evs[2 * j + 2].record()
-        host = stats.cpu().numpy()
-        self._sync_rng()
-        res = []
-        for j in range(steps):
-            st = _decode_stats(host[j])
-            if st["status"] == -1:
-                break
-            force_ms = evs[2 * j].elapsed_time(evs[2 * j + 1])
-            maint_ms = evs[2 * j + 1].elapsed_time(evs[2 * j + 2])
-            _raise_for(st, self.step_index)
-            flags = self.last_overlap_flags.copy() if self.collect_flags else None
-            res.append(StepStats(step=self.step_index, dt_used=st["dt_used"],
-                                 overlap_iterations=st["overlap_iterations"], flip_passes=st["flip_passes"],
-                                 inversion_repairs=st["inversion_repairs"], rollbacks=st["rollbacks"],
-                                 n_overlapping=st["n_overlapping"], force_ms=force_ms, maintain_ms=maint_ms,
-                                 overlap_ms=0.0, step_ms=force_ms + maint_ms, overlap_flags=flags))
-            self.step_index += 1
-        return res
+    The list covers max(r_cutoff, sigma) + skin and is rebuilt on the device
+    once any particle moved more than skin/2 since the snapshot; overlap
+    candidates are the pairs within sigma + skin at build time."""
+
+    def __init__(self, sys: ParticleSystem, params: SimParams, rng=None, skin: float | None = None,
+                 debug_scan: bool = False, collect_flags: bool = False):
+        super().__init__(sys, params, rng, debug_scan, collect_flags)
+        if params.r_cutoff is None:
+            raise BrownsimError("short-range simulation requires r_cutoff")
+        self.skin = 0.5 * params.sigma if skin is None else float(skin)
+        self.r_list = max(params.r_cutoff, params.sigma) + self.skin
+        self.overlap_margin = params.sigma + self.skin
+        self.tri = None
+        self.bparams = make_params(params, sys.box.length, self.rng.seed, self.rng.stream, _abi.BD_FORCE_SR,
+                                   _abi.BD_LR_EXACT, self.skin, pairs=True)
+        self._eng = _Engine(sys, None, self.bparams, self.rng.call)
+        self._eng.clear_status()
+
+    @property
+    def verlet(self):
+        """The current device Verlet list (pair_a, pair_b, snapshot) or None before the first step."""
+        from .forces import VerletList
+        meta = self._eng.vl_meta.cpu().numpy()
+        if not meta[1]:
+            return None
+        k = int(meta[0])
+        return VerletList(self._eng.pair_a[:k], self._eng.pair_b[:k], self._eng.vl_snap, self.r_list, self.skin)
+
+    def _launch_driver(self, stats_ptr: int):
+        check(lib().bd_step_verlet(ctypes.byref(self._eng.s), ctypes.byref(self.bparams),
+                                   ctypes.c_void_p(stats_ptr), _stream()), "bd_step_verlet")

@@ -49,6 +49,58 @@ def long_range_kernel(pos, alpha, mu, L, tile=32, precision="exact"):
     return out.cpu().numpy(), err.cpu().numpy()
 
 
+def short_range_kernel(pos, alpha, mu, pair_a, pair_b, L, r_cutoff):
+    """_kernels.short_range_kernel (_kernels.py:62-91), bit-exact (per-particle
+    gather in ascending pair order)."""
+    torch = require_cuda()
+    pos_t, a_t, m_t = _dev(pos, np.float64), _dev(alpha, np.float64), _dev(mu, np.float64)
+    pa, pb = _dev(pair_a, np.int64), _dev(pair_b, np.int64)
+    n, P = pos_t.shape[0], pa.shape[0]
+    out = torch.empty((n, 2), dtype=torch.float64, device=pos_t.device)
+    err = torch.empty(n, dtype=torch.int64, device=pos_t.device)
+    work = torch.empty(lib().bd_pairs_workspace_bytes(n, float(L), 0.0, max(P, 1)) // 8 + 64, dtype=torch.int64,
+                       device=pos_t.device)
+    check(lib().bd_short_range_forces(pos_t.data_ptr(), a_t.data_ptr(), m_t.data_ptr(), n, pa.data_ptr(),
+                                      pb.data_ptr(), P, float(L), float(r_cutoff), out.data_ptr(), err.data_ptr(),
+                                      work.data_ptr(), _stream()), "bd_short_range_forces")
+    return out.cpu().numpy(), err.cpu().numpy()
+
+
+def overlap_pass_kernel(pos, pair_a, pair_b, L, sigma, resolve_frac):
+    """_kernels.overlap_pass_kernel (_kernels.py:94-125): (disp, flags, count)."""
+    torch = require_cuda()
+    pos_t = _dev(pos, np.float64)
+    pa, pb = _dev(pair_a, np.int64), _dev(pair_b, np.int64)
+    n, P = pos_t.shape[0], pa.shape[0]
+    disp = torch.empty((n, 2), dtype=torch.float64, device=pos_t.device)
+    flags = torch.empty(n, dtype=torch.uint8, device=pos_t.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=pos_t.device)
+    work = torch.empty(lib().bd_pairs_workspace_bytes(n, float(L), 0.0, max(P, 1)) // 8 + 64, dtype=torch.int64,
+                       device=pos_t.device)
+    check(lib().bd_overlap_pass(pos_t.data_ptr(), n, pa.data_ptr(), pb.data_ptr(), P, float(L), float(sigma),
+                                float(resolve_frac), disp.data_ptr(), flags.data_ptr(), cnt.data_ptr(),
+                                work.data_ptr(), _stream()), "bd_overlap_pass")
+    return disp.cpu().numpy(), flags.cpu().numpy().astype(bool), int(cnt.item())
+
+
+def max_sq_displacement(pos, snapshot, L):
+    """_kernels.max_sq_displacement (_kernels.py:128-138)."""
+    torch = require_cuda()
+    p, s = _dev(pos, np.float64), _dev(snapshot, np.float64)
+    out = torch.zeros(1, dtype=torch.float64, device=p.device)
+    check(lib().bd_max_sq_displacement(p.data_ptr(), s.data_ptr(), p.shape[0], float(L), out.data_ptr(), _stream()),
+          "bd_max_sq_displacement")
+    return float(out.item())
+
+
+def verlet_pairs(pos, L, r_list):
+    """build_cell_grid + cell_pairs (forces.py:120-142): the ordered pair list."""
+    from .core import PeriodicBox
+    from .forces import build_verlet
+    vl = build_verlet(_dev(pos, np.float64), PeriodicBox(float(L)), float(r_list), 0.0)
+    return vl.pair_a.cpu().numpy(), vl.pair_b.cpu().numpy()
+
+
 def normals(seed: int, stream: int, call: int, n_pairs: int, purpose: int = 0) -> np.ndarray:
     """(n_pairs, 2) counter-based standard normals of one call."""
     torch = require_cuda()

@@ -196,8 +196,30 @@ def kernel_fixtures():
     print("kernels.npz written")
 
 
+def build_fixtures():
+    """Reference one-time triangulation build (triangulation.py:514-648):
+    the quotient arrays before the clean-up flips, and the final arrays."""
+    from brownsim.triangulation import _JITTER_KEY, _build_from_tiling
+    rec = {}
+    for tag, n, rho, seed in (("a", 256, 0.3, 0), ("b", 1000, 0.6, 1)):
+        sys_, box = make_system(n, rho, C0, seed)
+        pos = sys_.positions.copy()
+        gen = np.random.Generator(np.random.Philox(key=np.array(_JITTER_KEY, dtype=np.uint64)))
+        jit = pos + gen.standard_normal((n, 2)) * (1e-9 * box.length)
+        pre = _build_from_tiling(jit, box, n, 1, 1e-12)
+        fin = build_initial(pos, box)
+        rec[f"{tag}_pos"] = pos
+        rec[f"{tag}_L"] = box.length
+        for k in TRI_KEYS:
+            rec[f"{tag}_pre_{k}"] = getattr(pre, k)
+            rec[f"{tag}_fin_{k}"] = getattr(fin, k)
+    np.savez_compressed(os.path.join(HERE, "build.npz"), **rec)
+    print("build.npz written")
+
+
 def main():
     kernel_fixtures()
+    build_fixtures()
     run_scenario("lr_c0_n256", 256, 0.3, C0, 0, 30)
     run_scenario("lr_c3_n512", 512, 0.3, C3, 1, 30)
     run_scenario("lr_rollback_n64", 64, 0.35, [(0.5, 3.0, 3.0), (0.5, -3.0, -3.0)], 0, 3, dt=10.0)

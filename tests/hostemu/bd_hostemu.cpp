@@ -1,21 +1,31 @@
-// bd_hostemu.cpp -- TEST HARNESS: the product's step driver compiled for the host.
+// bd_hostemu.cpp -- TEST HARNESS: the product's step drivers compiled for the host.
 //
-// Compiles paper_1703_02484_b200/csrc/bd_step.cuh (the exact source the GPU
-// runs) with the ExecHost policy: one host thread walks every phase in
+// Compiles paper_1703_02484_b200/csrc/bd_drivers.cuh (the exact source the
+// GPU runs) with the ExecHost policy: one host thread walks every phase in
 // order, barriers are no-ops.  This lets the CPU test suite check the
-// driver's control flow and arithmetic (LFMIS flip selection, incidence
-// gathers, rollback, crossings bookkeeping) against the oracle without a
-// GPU.  It is loaded only by tests/; the product never uses it.
+// drivers' control flow and arithmetic (LFMIS flip selection, incidence
+// gathers, Verlet pair order, rollback, crossings bookkeeping) against the
+// oracle without a GPU.  It is loaded only by tests/; the product never
+// uses it.
 #include "../../paper_1703_02484_b200/csrc/bd_allpairs.cuh"
-#include "../../paper_1703_02484_b200/csrc/bd_step.cuh"
+#include "../../paper_1703_02484_b200/csrc/bd_drivers.cuh"
 
 using namespace bd;
+
+static Ctx host_ctx(const bd_state_t* s, const bd_params_t* p) {
+    Ctx c;
+    c.p = *p;
+    c.s = *s;
+    c.w = ws_carve(s->work, *p, s->tri.ne, s->tri.nt);
+    c.call = s->call ? *s->call : 0;
+    return c;
+}
 
 extern "C" {
 
 void bdh_prepare_params(bd_params_t* p) { prepare_params(p); }
 
-int64_t bdh_workspace_bytes(int64_t n, int64_t ne, int64_t nt) { return ws_layout(n, ne, nt).total; }
+int64_t bdh_workspace_bytes(const bd_params_t* p, int64_t ne, int64_t nt) { return ws_layout(*p, ne, nt).total; }
 
 double bdh_mi_fast(double d, const bd_params_t* p) { return mi_fast(d, p->L, p->mi_lo, p->mi_hi); }
 double bdh_mi_ref(double d, double L) { return mi_ref(d, L); }
@@ -29,27 +39,44 @@ void bdh_long_range(const bd_state_t* s, const bd_params_t* p) {
         lr_receiver_exact(s->pos, s->alpha, s->mu, p->n, p->L, p->mi_lo, p->mi_hi, i, s->force, s->force_err);
 }
 
+// the selector form of the all-pairs loop (the GPU kernel's image decision)
+void bdh_long_range_selector(const double* pos, const double* alpha, const double* mu, int64_t n,
+                             const bd_params_t* p, double* out, int64_t* err) {
+    for (int64_t i = 0; i < n; ++i)
+        lr_receiver_selector(pos, alpha, mu, n, p->L, p->mi_lo, p->mi_hi, i, out, err);
+}
+
 void bdh_step_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out) {
-    bdh_long_range(s, p);
-    Ctx c;
-    c.p = *p;
-    c.s = *s;
-    c.w = ws_carve(s->work, p->n, s->tri.ne, s->tri.nt);
-    c.call = *s->call;
+    if (p->force_mode != BD_FORCE_SR) bdh_long_range(s, p);
+    Ctx c = host_ctx(s, p);
     ExecHost x{c.w.ctl};
     step_tri_after_force(x, c, out);
 }
 
+void bdh_step_verlet(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out) {
+    Ctx c = host_ctx(s, p);
+    ExecHost x{c.w.ctl};
+    step_verlet(x, c, out);
+}
+
 int64_t bdh_restore_delaunay(const bd_state_t* s, const bd_params_t* p) {
-    Ctx c;
-    c.p = *p;
-    c.s = *s;
-    c.w = ws_carve(s->work, p->n, s->tri.ne, s->tri.nt);
+    Ctx c = host_ctx(s, p);
     c.call = 0;
     ExecHost x{c.w.ctl};
     Red<ExecHost> R(x);
     for (int k = 0; k < 8; ++k) c.w.ctl->red[k] = 0;
     return restore_delaunay(x, R, c, 1000);
+}
+
+// Verlet build only (pairs into s->pair_a/pair_b); returns the pair count
+int64_t bdh_verlet_build(const bd_state_t* s, const bd_params_t* p, double margin) {
+    Ctx c = host_ctx(s, p);
+    ExecHost x{c.w.ctl};
+    Red<ExecHost> R(x);
+    for (int k = 0; k < 8; ++k) c.w.ctl->red[k] = 0;
+    c.w.ctl->status = 0;
+    if (!vl_rebuild(x, R, c, margin)) return -1;
+    return c.s.vl_meta[0];
 }
 
 }  // extern "C"

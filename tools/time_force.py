@@ -1,0 +1,36 @@
+"""Time the all-pairs force alone (CUDA events) at N, for quick kernel iteration."""
+import sys, os, ctypes
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_1703_02484_b200._lib import lib
+from paper_1703_02484_b200 import kernels
+
+for spec in sys.argv[1:] or ["131072:fast"]:
+    n, prec = spec.split(":")
+    n = int(n)
+    L = float(np.sqrt(n * np.pi * 0.25 / 0.3))
+    rng = np.random.default_rng(0)
+    pos = torch.from_numpy(rng.uniform(0, L, size=(n, 2))).cuda()
+    t = rng.integers(0, 2, n)
+    alpha = torch.from_numpy(np.where(t == 0, 3.0, -3.0)).cuda()
+    mu = torch.from_numpy(np.where(t == 0, 3.0, -1.5)).cuda()
+    out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    err = torch.empty(n, dtype=torch.int64, device="cuda")
+    work = torch.empty(lib().bd_long_range_workspace_bytes(n) // 8 + 8, dtype=torch.int64, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    p = 1 if prec == "fast" else 0
+    call = lambda: lib().bd_long_range_forces(pos.data_ptr(), alpha.data_ptr(), mu.data_ptr(), n, L, 0, n, p,
+                                             out.data_ptr(), err.data_ptr(), work.data_ptr(), st)
+    for _ in range(2):
+        call()
+    torch.cuda.synchronize()
+    reps = 5
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    print(f"n={n} {prec}: {ms:.3f} ms/force  {n*(n-1)/ms/1e9:.3f} Gpairs/ms-> {n*(n-1)/(ms*1e-3):.3e} pairs/s")
