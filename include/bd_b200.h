@@ -160,6 +160,19 @@ int bd_normals(uint64_t seed, uint64_t stream_id, uint64_t call, uint64_t purpos
  * (dynamics.py:194) for p->force_mode; writes s->force and s->force_err */
 int bd_force(const bd_state_t* s, const bd_params_t* p, void* stream);
 
+/* The same force in three calls, for sharding across GPUs (one process per
+ * GPU, all holding the full state): every rank runs _prepare (sort + pack of
+ * the sources), _slots for its own receiver slots [s0, s1) -- records
+ * (fx, fy, flag) written to slot3[3*s .. 3*s+2] --, then the records of all
+ * slots are all-gathered (NCCL) into one (n, 3) array and _finish scatters
+ * them into s->force / s->force_err.  Slot order is the sorted order of the
+ * FAST path and particle order for EXACT; each receiver's sum is computed
+ * whole by one rank, so the result is bit-identical for every rank count. */
+int bd_force_prepare(const bd_state_t* s, const bd_params_t* p, void* stream);
+int bd_force_slots(const bd_state_t* s, const bd_params_t* p, int64_t s0, int64_t s1, double* slot3,
+                   void* stream);
+int bd_force_finish(const bd_state_t* s, const bd_params_t* p, const double* slot3, void* stream);
+
 /* the rest of LongRangeSimulation.step after the force (dynamics.py:196-274):
  * integrate, pass-through check, inversion repair, Delaunay restoration,
  * overlap correction with the joint fixed point, rollback -- one persistent

@@ -42,8 +42,7 @@ struct SortWs {
     int32_t* order;     // (n) sorted slot -> particle
     Src6* src;          // (n) packed sources in slot order
     uint64_t* bbox;     // (ntiles, 4) min/max bits of x and y per tile
-    double* fslot;      // (n, 2) forces per slot
-    int64_t* eslot;     // (n) err per slot (0 / -1)
+    double* slot3;      // (n, 3) per slot: fx, fy, flag (0 ok / -1 exact re-scan)
     int32_t grid_log2;  // cells per axis = 2^grid_log2
 };
 
@@ -61,7 +60,7 @@ BD_HD int64_t fs_align(int64_t x) { return (x + 255) & ~(int64_t)255; }
 BD_HD int64_t fast_ws_bytes(int64_t n) {
     const int64_t nc = fast_ncells(n), nt = (n + FS_TS - 1) / FS_TS;
     return fs_align(4 * n) + fs_align(4 * (nc + 1)) + fs_align(4 * nc) + fs_align(4 * n) + fs_align(48 * n) +
-           fs_align(32 * nt) + fs_align(16 * n) + fs_align(8 * n) + 256;
+           fs_align(32 * nt) + fs_align(24 * n) + 256;
 }
 
 BD_HD SortWs fast_ws_carve(void* base, int64_t n) {
@@ -75,8 +74,7 @@ BD_HD SortWs fast_ws_carve(void* base, int64_t n) {
     w.order = (int32_t*)b; b += fs_align(4 * n);
     w.src = (Src6*)b; b += fs_align(48 * n);
     w.bbox = (uint64_t*)b; b += fs_align(32 * nt);
-    w.fslot = (double*)b; b += fs_align(16 * n);
-    w.eslot = (int64_t*)b;
+    w.slot3 = (double*)b;
     return w;
 }
 
@@ -254,7 +252,8 @@ constexpr int FS_RPB = FS_BT * FS_R;     // receivers per CTA
 // receivers = sorted slots [i0, i1); CTA b owns [i0 + b*FS_RPB, +FS_RPB),
 // thread t the slots t and t + FS_BT of it
 __global__ void __launch_bounds__(FS_BT, 8)
-    k_allpairs_fast(SortWs w, int64_t n, double L, double lo, double hi, int64_t i0, int64_t i1) {
+    k_allpairs_fast(SortWs w, int64_t n, double L, double lo, double hi, int64_t i0, int64_t i1,
+                    double* __restrict__ slot3) {
     __shared__ __align__(128) Src6 tile[2][FS_TS];
     __shared__ __align__(8) uint64_t bars[2];
     constexpr int R = FS_R;
@@ -362,19 +361,39 @@ __global__ void __launch_bounds__(FS_BT, 8)
         if (!act[m]) continue;
         const int64_t slot = r.slot[m];
         const double fx = mux[m] * r.fx[m], fy = mux[m] * r.fy[m];
-        w.fslot[2 * slot] = fx;
-        w.fslot[2 * slot + 1] = fy;
-        w.eslot[slot] = (isfinite(fx) && isfinite(fy) && e[m] == 0) ? 0 : -1;  // -1: exact re-scan
+        slot3[3 * slot] = fx;
+        slot3[3 * slot + 1] = fy;
+        slot3[3 * slot + 2] = (isfinite(fx) && isfinite(fy) && e[m] == 0) ? 0.0 : -1.0;  // -1: exact re-scan
     }
 }
 
 // slot results -> particle order
-__global__ void k_unsort_forces(int64_t s0, int64_t s1, SortWs w, double* __restrict__ out, int64_t* __restrict__ err) {
+__global__ void k_unsort_forces(int64_t s0, int64_t s1, SortWs w, const double* __restrict__ slot3,
+                                double* __restrict__ out, int64_t* __restrict__ err) {
     for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s1; s += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = w.order[s];
-        out[2 * i] = w.fslot[2 * s];
-        out[2 * i + 1] = w.fslot[2 * s + 1];
-        err[i] = w.eslot[s];
+        out[2 * i] = slot3[3 * s];
+        out[2 * i + 1] = slot3[3 * s + 1];
+        err[i] = (int64_t)slot3[3 * s + 2];
+    }
+}
+
+// EXACT sharded path: receivers [s0, s1) of force/err (particle order) -> slot records
+__global__ void k_pack_slot3(int64_t s0, int64_t s1, const double* __restrict__ force, const int64_t* __restrict__ err,
+                             double* __restrict__ slot3) {
+    for (int64_t i = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s1; i += (int64_t)gridDim.x * blockDim.x) {
+        slot3[3 * i] = force[2 * i];
+        slot3[3 * i + 1] = force[2 * i + 1];
+        slot3[3 * i + 2] = (double)err[i];
+    }
+}
+
+__global__ void k_unpack_slot3(int64_t n, const double* __restrict__ slot3, double* __restrict__ force,
+                               int64_t* __restrict__ err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        force[2 * i] = slot3[3 * i];
+        force[2 * i + 1] = slot3[3 * i + 1];
+        err[i] = (int64_t)slot3[3 * i + 2];
     }
 }
 

@@ -314,17 +314,18 @@ int launch_fast_prepare(const double* pos, const double* alpha, const double* mu
 }
 
 // FAST stage 2: receivers = sorted slots [s0, s1)
-int launch_fast_slots(int64_t n, const bd_params_t& p, int64_t s0, int64_t s1, const SortWs& w, cudaStream_t st) {
+int launch_fast_slots(int64_t n, const bd_params_t& p, int64_t s0, int64_t s1, const SortWs& w, double* slot3,
+                      cudaStream_t st) {
     if (s1 <= s0) return 0;
     const int64_t nb = (s1 - s0 + FS_RPB - 1) / FS_RPB;
-    k_allpairs_fast<<<(unsigned)nb, FS_BT, 0, st>>>(w, n, p.L, p.mi_lo, p.mi_hi, s0, s1);
+    k_allpairs_fast<<<(unsigned)nb, FS_BT, 0, st>>>(w, n, p.L, p.mi_lo, p.mi_hi, s0, s1, slot3);
     return err_code(cudaGetLastError());
 }
 
 // FAST stage 3: slots -> particle order; exact re-scan of flagged receivers
-int launch_fast_finish(const double* pos, int64_t n, const bd_params_t& p, const SortWs& w, double* out,
-                       int64_t* err, cudaStream_t st) {
-    k_unsort_forces<<<grid_for(n), 256, 0, st>>>(0, n, w, out, err);
+int launch_fast_finish(const double* pos, int64_t n, const bd_params_t& p, const SortWs& w, const double* slot3,
+                       double* out, int64_t* err, cudaStream_t st) {
+    k_unsort_forces<<<grid_for(n), 256, 0, st>>>(0, n, w, slot3, out, err);
     k_lr_rescan_pos<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, p.mi_lo, p.mi_hi, err);
     return err_code(cudaGetLastError());
 }
@@ -338,9 +339,9 @@ int launch_force(const bd_state_t* s, const bd_params_t* p, cudaStream_t st) {
         const SortWs fw = fast_ws_carve(w.src4, p->n);
         int rc = launch_fast_prepare(s->pos, s->alpha, s->mu, p->n, p->L, fw, st);
         if (rc) return rc;
-        rc = launch_fast_slots(p->n, *p, 0, p->n, fw, st);
+        rc = launch_fast_slots(p->n, *p, 0, p->n, fw, fw.slot3, st);
         if (rc) return rc;
-        return launch_fast_finish(s->pos, p->n, *p, fw, s->force, s->force_err, st);
+        return launch_fast_finish(s->pos, p->n, *p, fw, fw.slot3, s->force, s->force_err, st);
     }
     int rc = launch_pack(s->pos, s->alpha, p->n, (double4*)w.src4, st);
     if (rc) return rc;
@@ -444,9 +445,9 @@ int bd_long_range_forces(const double* pos, const double* alpha, const double* m
         const SortWs fw = fast_ws_carve(work, n);
         int rc = launch_fast_prepare(pos, alpha, mu, n, L, fw, st);
         if (rc) return rc;
-        rc = launch_fast_slots(n, p, 0, n, fw, st);
+        rc = launch_fast_slots(n, p, 0, n, fw, fw.slot3, st);
         if (rc) return rc;
-        return launch_fast_finish(pos, n, p, fw, out, err, st);
+        return launch_fast_finish(pos, n, p, fw, fw.slot3, out, err, st);
     }
     int rc = launch_pack(pos, alpha, n, (double4*)work, st);
     if (rc) return rc;
@@ -516,6 +517,43 @@ int bd_normals(uint64_t seed, uint64_t stream_id, uint64_t call, uint64_t purpos
 
 int bd_force(const bd_state_t* s, const bd_params_t* p, void* stream) {
     return launch_force(s, p, (cudaStream_t)stream);
+}
+
+// ---- sharded all-pairs force (multi-GPU: receiver slots per rank + all-gather)
+int bd_force_prepare(const bd_state_t* s, const bd_params_t* p, void* stream) {
+    init_device_info();
+    cudaStream_t st = (cudaStream_t)stream;
+    if (p->force_mode == BD_FORCE_SR) return 0;
+    const Ws w = ws_carve(s->work, *p, s->tri.ne, s->tri.nt);
+    if (p->lr_precision == BD_LR_FAST)
+        return launch_fast_prepare(s->pos, s->alpha, s->mu, p->n, p->L, fast_ws_carve(w.src4, p->n), st);
+    return launch_pack(s->pos, s->alpha, p->n, (double4*)w.src4, st);
+}
+
+int bd_force_slots(const bd_state_t* s, const bd_params_t* p, int64_t s0, int64_t s1, double* slot3, void* stream) {
+    init_device_info();
+    cudaStream_t st = (cudaStream_t)stream;
+    if (p->force_mode == BD_FORCE_SR) return 0;
+    if (s1 > p->n) s1 = p->n;
+    if (s1 <= s0) return 0;
+    const Ws w = ws_carve(s->work, *p, s->tri.ne, s->tri.nt);
+    if (p->lr_precision == BD_LR_FAST)
+        return launch_fast_slots(p->n, *p, s0, s1, fast_ws_carve(w.src4, p->n), slot3, st);
+    int rc = launch_lr((const double4*)w.src4, s->mu, p->n, *p, s0, s1, BD_LR_EXACT, s->force, s->force_err, st);
+    if (rc) return rc;
+    k_pack_slot3<<<grid_for(s1 - s0), 256, 0, st>>>(s0, s1, s->force, s->force_err, slot3);
+    return err_code(cudaGetLastError());
+}
+
+int bd_force_finish(const bd_state_t* s, const bd_params_t* p, const double* slot3, void* stream) {
+    init_device_info();
+    cudaStream_t st = (cudaStream_t)stream;
+    if (p->force_mode == BD_FORCE_SR) return 0;
+    const Ws w = ws_carve(s->work, *p, s->tri.ne, s->tri.nt);
+    if (p->lr_precision == BD_LR_FAST)
+        return launch_fast_finish(s->pos, p->n, *p, fast_ws_carve(w.src4, p->n), slot3, s->force, s->force_err, st);
+    k_unpack_slot3<<<grid_for(p->n), 256, 0, st>>>(p->n, slot3, s->force, s->force_err);
+    return err_code(cudaGetLastError());
 }
 
 int bd_maintain_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, void* stream) {

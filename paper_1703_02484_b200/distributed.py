@@ -1,0 +1,113 @@
+"""Multi-GPU sharding of the all-pairs force (one process per GPU).
+
+Only the O(N^2) force is partitioned: every rank holds the
+full simulation state, computes the forces of its own contiguous block of
+receiver slots, and the (fx, fy, flag) records of all slots are all-gathered
+over NCCL (NVLink/NVSwitch) into one (n, 3) buffer that every rank scatters
+into its force array.  The O(N) path -- integrate, triangulation
+maintenance, Verlet lists, overlap correction -- then runs as identical,
+deterministic replicas on every rank, so no further collective is needed
+(its per-pass global barriers would cost more over NVLink than the work;
+DESIGN.md §Multi-GPU).  Each receiver's sum is computed whole by one rank
+in the same order, so results are bit-identical for any world size.
+
+Per step the collective moves 24 B x N (3 MiB at N = 131,072).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+from ._lib import check, lib
+
+
+@dataclass
+class Shard:
+    rank: int
+    world: int
+    chunk: int  # slots per rank (last rank may own fewer)
+
+    def bounds(self, n: int):
+        s0 = min(n, self.rank * self.chunk)
+        return s0, min(n, s0 + self.chunk)
+
+
+def shard_for(n: int, rank: int, world: int) -> Shard:
+    return Shard(rank, world, (n + world - 1) // world)
+
+
+class ShardedLongRange:
+    """Receiver-slot sharding of the all-pairs force over a process group.
+
+    `gather(buf, mine)` must all-gather `mine` (a view of `buf` at this rank's
+    offset) into `buf`; by default torch.distributed.all_gather_into_tensor on
+    the given group (NCCL on GPUs)."""
+
+    def __init__(self, rank: int, world: int, group=None, gather=None):
+        self.rank = int(rank)
+        self.world = int(world)
+        self.group = group
+        self._gather = gather
+        self._buf = None
+
+    @classmethod
+    def from_env(cls, group=None):
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            return cls(dist.get_rank(group), dist.get_world_size(group), group)
+        return cls(int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), group)
+
+    def gather(self, buf, mine):
+        if self._gather is not None:
+            return self._gather(buf, mine)
+        import torch.distributed as dist
+        dist.all_gather_into_tensor(buf, mine, group=self.group)
+
+    def buffer(self, n: int, device):
+        import torch
+        sh = shard_for(n, self.rank, self.world)
+        rows = sh.chunk * self.world
+        if self._buf is None or self._buf.shape[0] != rows or self._buf.device != device:
+            self._buf = torch.zeros((rows, 3), dtype=torch.float64, device=device)
+        return self._buf, sh
+
+    def force(self, state, params, stream):
+        """bd_force for a sharded group: prepare, own slots, all-gather, finish."""
+        n = int(params.n)
+        buf, sh = self.buffer(n, self._device_of(state))
+        s0, s1 = sh.bounds(n)
+        L = lib()
+        check(L.bd_force_prepare(ctypes.byref(state), ctypes.byref(params), stream), "bd_force_prepare")
+        check(L.bd_force_slots(ctypes.byref(state), ctypes.byref(params), s0, s1, ctypes.c_void_p(buf.data_ptr()),
+                               stream), "bd_force_slots")
+        mine = buf[self.rank * sh.chunk:(self.rank + 1) * sh.chunk]
+        self.gather(buf, mine)
+        check(L.bd_force_finish(ctypes.byref(state), ctypes.byref(params), ctypes.c_void_p(buf.data_ptr()), stream),
+              "bd_force_finish")
+
+    def _device_of(self, state):
+        import torch
+        return torch.device("cuda", torch.cuda.current_device())
+
+
+class SequentialShards(ShardedLongRange):
+    """All `world` shards computed one after another on this GPU (the
+    single-GPU check of the sharded path: same slices, same buffer layout,
+    the all-gather replaced by the identity)."""
+
+    def __init__(self, world: int):
+        super().__init__(0, world, gather=lambda buf, mine: None)
+
+    def force(self, state, params, stream):
+        n = int(params.n)
+        buf, _ = self.buffer(n, self._device_of(state))
+        L = lib()
+        check(L.bd_force_prepare(ctypes.byref(state), ctypes.byref(params), stream), "bd_force_prepare")
+        for r in range(self.world):
+            s0, s1 = shard_for(n, r, self.world).bounds(n)
+            check(L.bd_force_slots(ctypes.byref(state), ctypes.byref(params), s0, s1,
+                                   ctypes.c_void_p(buf.data_ptr()), stream), "bd_force_slots")
+        check(L.bd_force_finish(ctypes.byref(state), ctypes.byref(params), ctypes.c_void_p(buf.data_ptr()), stream),
+              "bd_force_finish")

@@ -281,8 +281,9 @@ class LongRangeSimulation(_SimulationBase):
 
     def __init__(self, sys: ParticleSystem, params: SimParams, rng=None, tri: PeriodicTriangulation | None = None,
                  debug_scan: bool = False, collect_flags: bool = False, force: str = "long-range",
-                 precision: str = "exact", skin: float | None = None):
+                 precision: str = "exact", skin: float | None = None, sharding=None):
         super().__init__(sys, params, rng, debug_scan, collect_flags)
+        self.sharding = sharding  # distributed.ShardedLongRange: multi-GPU all-pairs
         if tri is None:
             from .triangulation import build_initial
             tri = build_initial(sys.positions, sys.box, device=sys.device)
@@ -302,6 +303,9 @@ class LongRangeSimulation(_SimulationBase):
         self._eng.clear_status()
 
     def _launch_force(self):
+        if self.sharding is not None and self.sharding.world > 1:
+            self.sharding.force(self._eng.s, self.bparams, _stream())
+            return
         check(lib().bd_force(ctypes.byref(self._eng.s), ctypes.byref(self.bparams), _stream()), "bd_force")
 
     def _launch_driver(self, stats_ptr: int):
