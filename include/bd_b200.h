@@ -150,6 +150,11 @@ int bd_max_sq_displacement(const double* pos, const double* snap, int64_t n, dou
 int bd_verlet_build(const double* pos, int64_t n, double L, double r_list, int64_t* pair_a,
                     int64_t* pair_b, int64_t capacity, int64_t* count, void* work, void* stream);
 
+/* brute_force_overlaps (_kernels.py:239-275), the O(N^2) debug oracle of
+ * run(debug_scan=True): out[0] = number of pairs a < b closer than thresh,
+ * out[1] = (a << 32) | b of the first such pair (or all ones) */
+int bd_brute_overlaps(const double* pos, int64_t n, double L, double thresh, int64_t* out, void* stream);
+
 /* counter-based normals for pairs [0, n_pairs) of one call */
 int bd_normals(uint64_t seed, uint64_t stream_id, uint64_t call, uint64_t purpose, int64_t n_pairs,
                double* out, void* stream);

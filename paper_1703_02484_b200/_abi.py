@@ -73,6 +73,7 @@ def _protos():
         "bd_max_sq_displacement": ([c_vp, c_vp, c_i64, c_d, c_vp, c_vp], c_int),
         "bd_verlet_build": ([c_vp, c_i64, c_d, c_d, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp], c_int),
         "bd_probe_fp64": ([c_i64, c_vp, c_vp, P(c_d)], c_int),
+        "bd_brute_overlaps": ([c_vp, c_i64, c_d, c_d, c_vp, c_vp], c_int),
         "bd_normals": ([c_u64, c_u64, c_u64, c_u64, c_i64, c_vp, c_vp], c_int),
         "bd_force": ([P(BdState), P(BdParams), c_vp], c_int),
         "bd_force_prepare": ([P(BdState), P(BdParams), c_vp], c_int),
@@ -101,7 +102,7 @@ def declare(lib):
 
 
 # every symbol the header declares (checked by tests/test_abi.py)
-EXPORTS = ("bd_force", "bd_force_prepare", "bd_force_slots", "bd_force_finish", "bd_maintain_tri", "bd_prepare_params", "bd_workspace_bytes", "bd_long_range_workspace_bytes",
+EXPORTS = ("bd_brute_overlaps", "bd_force","bd_force_prepare", "bd_force_slots", "bd_force_finish", "bd_maintain_tri", "bd_prepare_params", "bd_workspace_bytes", "bd_long_range_workspace_bytes",
            "bd_long_range_forces", "bd_short_range_forces", "bd_overlap_pass",
            "bd_max_sq_displacement", "bd_verlet_build", "bd_pairs_workspace_bytes", "bd_normals",
            "bd_step_tri", "bd_run_tri", "bd_step_verlet", "bd_run_verlet",

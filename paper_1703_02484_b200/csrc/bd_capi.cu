@@ -176,6 +176,28 @@ __global__ void k_max_sq_disp(const double* pos, const double* snap, int64_t n, 
     if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
 }
 
+// brute_force_overlaps (_kernels.py:239-275): every pair a < b with
+// |mi(pos_b - pos_a)|^2 < thresh^2; count and the lexicographically first pair
+__global__ void k_brute_overlaps(const double* pos, int64_t n, bd_params_t p, double thresh,
+                                 unsigned long long* out) {
+    const double t2 = thresh * thresh;
+    unsigned long long cnt = 0, first = ~0ull;
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x) {
+        for (int64_t b = a + 1; b < n; ++b) {
+            const double dx = mi_exact(pos[2 * b] - pos[2 * a], p), dy = mi_exact(pos[2 * b + 1] - pos[2 * a + 1], p);
+            if (dx * dx + dy * dy < t2) {
+                ++cnt;
+                const unsigned long long key = ((unsigned long long)a << 32) | (unsigned long long)b;
+                first = key < first ? key : first;
+            }
+        }
+    }
+    if (cnt) {
+        atomicAdd(&out[0], cnt);
+        atomicMin(&out[1], first);
+    }
+}
+
 __global__ void k_normals(uint64_t seed, uint64_t stream_id, uint64_t call, uint64_t purpose, int64_t npairs,
                           double* out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npairs; i += (int64_t)gridDim.x * blockDim.x) {
@@ -505,6 +527,20 @@ int bd_max_sq_displacement(const double* pos, const double* snap, int64_t n, dou
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), st);
     if (e != cudaSuccess) return err_code(e);
     k_max_sq_disp<<<grid_for(n), 256, 0, st>>>(pos, snap, n, p, (unsigned long long*)out);
+    return err_code(cudaGetLastError());
+}
+
+int bd_brute_overlaps(const double* pos, int64_t n, double L, double thresh, int64_t* out, void* stream) {
+    init_device_info();
+    bd_params_t p;
+    memset(&p, 0, sizeof(p));
+    p.L = L;
+    prepare_params(&p);
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned long long init[2] = {0ull, ~0ull};
+    cudaError_t e = cudaMemcpyAsync(out, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return err_code(e);
+    k_brute_overlaps<<<grid_for(n, 128), 128, 0, st>>>(pos, n, p, thresh, (unsigned long long*)out);
     return err_code(cudaGetLastError());
 }
 

@@ -61,8 +61,7 @@ class StepStats:
     overlap_flags: np.ndarray | None = field(default=None, repr=False)
 
 
-class MissedOverlapError(BrownsimError):
-    """Debug scan found an overlapping pair the neighbour provider missed (dynamics.py:69-70)."""
+from .validation import MissedOverlapError  # noqa: E402  (dynamics.py:69-70)
 
 
 def _tri_struct(tensors: dict, nv: int) -> _abi.BdTri:
