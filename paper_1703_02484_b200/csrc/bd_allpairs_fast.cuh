@@ -108,21 +108,22 @@ __global__ void k_sort_count(const double* __restrict__ pos, int64_t n, double L
 // single-CTA exclusive scan of the cell counts (<= 2^30 cells; one pass of
 // 1024-wide chunks with a running carry)
 __global__ void __launch_bounds__(1024) k_sort_scan(SortWs w, int64_t ncells) {
+    // each thread owns a contiguous run of cells: serial sums, one block
+    // scan of the 1024 run totals, serial write-back (3 barriers in total)
     __shared__ int64_t sh[32];
-    int64_t carry = 0;
-    for (int64_t base = 0; base < ncells; base += blockDim.x) {
-        const int64_t c = base + threadIdx.x;
-        const int64_t v = c < ncells ? w.cell_off[c] : 0;
-        int64_t ex;
-        const int64_t tot = block_excl_scan(v, ex, sh);
-        if (c < ncells) {
-            w.cell_off[c] = (int32_t)(carry + ex);
-            w.cell_cur[c] = 0;
-        }
-        carry += tot;
-        __syncthreads();
+    const int64_t per = (ncells + blockDim.x - 1) / blockDim.x;
+    const int64_t c0 = threadIdx.x * per, c1 = c0 + per < ncells ? c0 + per : ncells;
+    int64_t run = 0;
+    for (int64_t c = c0; c < c1; ++c) run += w.cell_off[c];
+    int64_t ex;
+    const int64_t tot = block_excl_scan(run, ex, sh);
+    for (int64_t c = c0; c < c1; ++c) {
+        const int32_t v = w.cell_off[c];
+        w.cell_off[c] = (int32_t)ex;
+        w.cell_cur[c] = 0;
+        ex += v;
     }
-    if (threadIdx.x == 0) w.cell_off[ncells] = (int32_t)carry;
+    if (threadIdx.x == 0) w.cell_off[ncells] = (int32_t)tot;
 }
 
 __global__ void k_sort_scatter(int64_t n, SortWs w) {
