@@ -43,8 +43,21 @@ struct SortWs {
     Src6* src;          // (n) packed sources in slot order
     uint64_t* bbox;     // (ntiles, 4) min/max bits of x and y per tile
     double* slot3;      // (n, 3) per slot: fx, fy, flag (0 ok / -1 exact re-scan)
+    double* part3;      // (splits, n, 3) per source partition: partial fx, fy, flag
     int32_t grid_log2;  // cells per axis = 2^grid_log2
+    int32_t splits;     // source partitions per receiver (fast_splits)
 };
+
+// Source partitions per receiver, a function of n ONLY (never of the GPU
+// count, so sharded results stay bit-identical for every world size): enough
+// (receiver, partition) work items for a full occupancy wave on one B200
+// even when 8 ranks share the receivers; capped at 16 and at half the tiles.
+BD_HD int fast_splits(int64_t n) {
+    const int64_t tiles = (n + 255) / 256;
+    int64_t s = 1;
+    while (s < 16 && n * s < (int64_t)148 * 1024 * 8 && 2 * s <= tiles) s *= 2;
+    return (int)s;
+}
 
 BD_HD int fast_grid_log2(int64_t n) {
     int g = 1;
@@ -60,7 +73,7 @@ BD_HD int64_t fs_align(int64_t x) { return (x + 255) & ~(int64_t)255; }
 BD_HD int64_t fast_ws_bytes(int64_t n) {
     const int64_t nc = fast_ncells(n), nt = (n + FS_TS - 1) / FS_TS;
     return fs_align(4 * n) + fs_align(4 * (nc + 1)) + fs_align(4 * nc) + fs_align(4 * n) + fs_align(48 * n) +
-           fs_align(32 * nt) + fs_align(24 * n) + 256;
+           fs_align(32 * nt) + fs_align(24 * n) + fs_align(24 * n * fast_splits(n)) + 256;
 }
 
 BD_HD SortWs fast_ws_carve(void* base, int64_t n) {
@@ -74,7 +87,9 @@ BD_HD SortWs fast_ws_carve(void* base, int64_t n) {
     w.order = (int32_t*)b; b += fs_align(4 * n);
     w.src = (Src6*)b; b += fs_align(48 * n);
     w.bbox = (uint64_t*)b; b += fs_align(32 * nt);
-    w.slot3 = (double*)b;
+    w.slot3 = (double*)b; b += fs_align(24 * n);
+    w.part3 = (double*)b;
+    w.splits = fast_splits(n);
     return w;
 }
 
@@ -289,7 +304,12 @@ __global__ void __launch_bounds__(FS_BT, 8)
 #pragma unroll
     for (int m = 0; m < R; ++m) e[m] = 0;
 
-    const int64_t ntiles = (n + FS_TS - 1) / FS_TS;
+    // this CTA's source partition: tiles [tb, te) of the sorted sources
+    const int64_t ntiles_all = (n + FS_TS - 1) / FS_TS;
+    const int64_t per_part = (ntiles_all + gridDim.y - 1) / gridDim.y;
+    const int64_t tb = (int64_t)blockIdx.y * per_part;
+    const int64_t te = tb + per_part < ntiles_all ? tb + per_part : ntiles_all;
+    const int64_t ntiles = te > tb ? te - tb : 0;
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -297,17 +317,19 @@ __global__ void __launch_bounds__(FS_BT, 8)
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int64_t t = 0; t < 2 && t < ntiles; ++t) {
+        for (int64_t u = 0; u < 2 && u < ntiles; ++u) {
+            const int64_t t = tb + u;
             const int64_t cnt = (t + 1) * FS_TS <= n ? FS_TS : n - t * FS_TS;
-            mbar_expect_tx(&bars[t], (uint32_t)(cnt * sizeof(Src6)));
-            bulk_g2s(&tile[t][0], w.src + t * FS_TS, (uint32_t)(cnt * sizeof(Src6)), &bars[t]);
+            mbar_expect_tx(&bars[u], (uint32_t)(cnt * sizeof(Src6)));
+            bulk_g2s(&tile[u][0], w.src + t * FS_TS, (uint32_t)(cnt * sizeof(Src6)), &bars[u]);
         }
     }
-    for (int64_t t = 0; t < ntiles; ++t) {
-        const int st = (int)(t & 1);
+    for (int64_t u = 0; u < ntiles; ++u) {
+        const int64_t t = tb + u;
+        const int st = (int)(u & 1);
         const uint64_t* bb = w.bbox + 4 * t;
         const uint64_t bx0 = bb[0], bx1 = bb[1], by0 = bb[2], by1 = bb[3];
-        mbar_wait(&bars[st], (uint32_t)((t >> 1) & 1));
+        mbar_wait(&bars[st], (uint32_t)((u >> 1) & 1));
         const Src6* sm = tile[st];
         const int64_t base = t * FS_TS;
         const int cnt = (int)((t + 1) * FS_TS <= n ? FS_TS : n - base);
@@ -350,7 +372,7 @@ __global__ void __launch_bounds__(FS_BT, 8)
             }
         }
         __syncthreads();
-        if (threadIdx.x == 0 && t + 2 < ntiles) {
+        if (threadIdx.x == 0 && u + 2 < ntiles) {
             const int64_t t2 = t + 2;
             const int64_t cnt2 = (t2 + 1) * FS_TS <= n ? FS_TS : n - t2 * FS_TS;
             mbar_expect_tx(&bars[st], (uint32_t)(cnt2 * sizeof(Src6)));
@@ -361,10 +383,36 @@ __global__ void __launch_bounds__(FS_BT, 8)
     for (int m = 0; m < R; ++m) {
         if (!act[m]) continue;
         const int64_t slot = r.slot[m];
-        const double fx = mux[m] * r.fx[m], fy = mux[m] * r.fy[m];
-        slot3[3 * slot] = fx;
-        slot3[3 * slot + 1] = fy;
-        slot3[3 * slot + 2] = (isfinite(fx) && isfinite(fy) && e[m] == 0) ? 0.0 : -1.0;  // -1: exact re-scan
+        if (gridDim.y == 1) {
+            const double fx = mux[m] * r.fx[m], fy = mux[m] * r.fy[m];
+            slot3[3 * slot] = fx;
+            slot3[3 * slot + 1] = fy;
+            slot3[3 * slot + 2] = (isfinite(fx) && isfinite(fy) && e[m] == 0) ? 0.0 : -1.0;  // -1: exact re-scan
+        } else {
+            double* o = w.part3 + 3 * ((int64_t)blockIdx.y * n + slot);
+            o[0] = r.fx[m];
+            o[1] = r.fy[m];
+            o[2] = e[m] == 0 ? 0.0 : -1.0;
+        }
+    }
+}
+
+// partial sums of the source partitions, added in partition order (deterministic)
+__global__ void k_reduce_parts(int64_t s0, int64_t s1, int64_t n, SortWs w, double* __restrict__ slot3) {
+    for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s1; s += (int64_t)gridDim.x * blockDim.x) {
+        double fx = 0.0, fy = 0.0, flag = 0.0;
+        for (int p = 0; p < w.splits; ++p) {
+            const double* o = w.part3 + 3 * ((int64_t)p * n + s);
+            fx += o[0];
+            fy += o[1];
+            flag = o[2] != 0.0 ? -1.0 : flag;
+        }
+        const double mu = w.src[s].mu;
+        fx = mu * fx;
+        fy = mu * fy;
+        slot3[3 * s] = fx;
+        slot3[3 * s + 1] = fy;
+        slot3[3 * s + 2] = (isfinite(fx) && isfinite(fy) && flag == 0.0) ? 0.0 : -1.0;
     }
 }
 

@@ -340,7 +340,9 @@ int launch_fast_slots(int64_t n, const bd_params_t& p, int64_t s0, int64_t s1, c
                       cudaStream_t st) {
     if (s1 <= s0) return 0;
     const int64_t nb = (s1 - s0 + FS_RPB - 1) / FS_RPB;
-    k_allpairs_fast<<<(unsigned)nb, FS_BT, 0, st>>>(w, n, p.L, p.mi_lo, p.mi_hi, s0, s1, slot3);
+    k_allpairs_fast<<<dim3((unsigned)nb, (unsigned)w.splits), FS_BT, 0, st>>>(w, n, p.L, p.mi_lo, p.mi_hi, s0, s1,
+                                                                               slot3);
+    if (w.splits > 1) k_reduce_parts<<<grid_for(s1 - s0), 256, 0, st>>>(s0, s1, n, w, slot3);
     return err_code(cudaGetLastError());
 }
 

@@ -34,3 +34,32 @@ for spec in sys.argv[1:] or ["131072:fast"]:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     print(f"n={n} {prec}: {ms:.3f} ms/force  {n*(n-1)/ms/1e9:.3f} Gpairs/ms-> {n*(n-1)/(ms*1e-3):.3e} pairs/s")
+
+# per-rank slice of the sharded force: slots [0, n/G) of a G-way split
+if os.environ.get("SLICES"):
+    import ctypes as C
+    from paper_1703_02484_b200 import _abi
+    from paper_1703_02484_b200.core import CounterRng, ParticleSystem, PeriodicBox, SimParams
+    from paper_1703_02484_b200.dynamics import make_params, _Engine
+    n = 131072
+    L = float(np.sqrt(n * np.pi * 0.25 / 0.3))
+    rng = np.random.default_rng(0)
+    pos = rng.uniform(0, L, size=(n, 2))
+    t = rng.integers(0, 2, n)
+    sys_ = ParticleSystem(pos, t, np.where(t == 0, 3.0, -3.0), np.where(t == 0, 3.0, -1.5), PeriodicBox(L))
+    bp = make_params(SimParams(n=n, sigma=1.0, dt=0.01, diffusion=0.01), L, 0, 2, 0, 1)
+    eng = _Engine(sys_, None, bp, 0)
+    buf = torch.zeros((n, 3), dtype=torch.float64, device="cuda")
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    lib().bd_force_prepare(C.byref(eng.s), C.byref(bp), st)
+    for G in (1, 2, 4, 8):
+        chunk = (n + G - 1) // G
+        call = lambda: lib().bd_force_slots(C.byref(eng.s), C.byref(bp), 0, chunk, C.c_void_p(buf.data_ptr()), st)
+        call(); torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            call()
+        e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 3
+        print(f"G={G}: per-rank slots force {ms:.3f} ms  (ideal {15.4 / G:.3f})")
