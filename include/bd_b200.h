@@ -208,6 +208,67 @@ int bd_run_verlet(const bd_state_t* s, const bd_params_t* p, int64_t steps, bd_s
 int bd_tri_restore_delaunay(const bd_state_t* s, const bd_params_t* p, int64_t* passes_out,
                             void* stream);
 
+/* ---- method boundary: the pieces of a step, one call each ------------
+ * The reference exposes the building blocks of a step as public functions
+ * and PeriodicTriangulation methods, and its tests drive them one by one.
+ * Each entry below runs the same device phase the fused step kernels use
+ * (csrc/bd_ops.cuh) as one cooperative launch on the state `s` (positions
+ * s->pos, previous positions s->prev, triangulation s->tri, scratch
+ * s->work).  `result` is a small device int64 array, layout per call. */
+
+/* dynamics.integrate (dynamics.py:73-94) with step dt: prev <- pos, then
+ * pos = wrap((pos + F dt) + xi sqrt(D dt)), xi = counter normals of call
+ * *s->call (which advances by one).  crossings (n,2) int64 (may be NULL);
+ * result = {status (0 / BD_ERR_STEPFAIL: non-finite force, nothing moved),
+ * particles that crossed, first bad particle} */
+int bd_integrate(const bd_state_t* s, const bd_params_t* p, double dt, int64_t* crossings,
+                 int64_t* result, void* stream);
+
+/* PeriodicTriangulation.apply_crossings (triangulation.py:166-177);
+ * crossings (n,2) int64 */
+int bd_tri_apply_crossings(const bd_state_t* s, const bd_params_t* p, const int64_t* crossings,
+                           void* stream);
+
+/* .edge_inversion_present(prev = s->prev, curr = s->pos) (triangulation.py:
+ * 240-250); result[0] = 0 / 1 */
+int bd_tri_edge_inversion(const bd_state_t* s, const bd_params_t* p, int64_t* result, void* stream);
+
+/* .signed_area2(s->pos) (triangulation.py:186-191): area (nt,) float64 */
+int bd_tri_signed_area2(const bd_state_t* s, const bd_params_t* p, double* area, void* stream);
+
+/* .delaunay_flags(s->pos, tol = p->tol) (triangulation.py:226-229) and
+ * .inverted_edge_flags(s->pos) (:231-234): flags (ne,) uint8 */
+int bd_tri_delaunay_flags(const bd_state_t* s, const bd_params_t* p, uint8_t* flags, void* stream);
+int bd_tri_inverted_edge_flags(const bd_state_t* s, const bd_params_t* p, uint8_t* flags, void* stream);
+
+/* .flip_edge(e) (triangulation.py:254-302) for edges[0..count) in order;
+ * result = {status (0 / BD_ERR_FLIP), index into edges of the failure} */
+int bd_tri_flip_edges(const bd_state_t* s, const bd_params_t* p, const int64_t* edges, int64_t count,
+                      int64_t* result, void* stream);
+
+/* .repair_inversions(s->pos, prev = s->prev if use_prev else None,
+ * max_passes) (triangulation.py:336-363);
+ * result = {status, flips, passes, needs_rollback} (RepairResult) */
+int bd_tri_repair_inversions(const bd_state_t* s, const bd_params_t* p, int64_t max_passes, int use_prev,
+                             int64_t* result, void* stream);
+
+/* .restore_delaunay(s->pos, tol = p->tol, max_passes) (triangulation.py:
+ * 319-334); result = {status (0 / BD_ERR_NONCONV / BD_ERR_FLIP), passes} */
+int bd_tri_restore_delaunay_ex(const bd_state_t* s, const bd_params_t* p, int64_t max_passes,
+                               int64_t* result, void* stream);
+
+/* dynamics.correct_overlaps (dynamics.py:97-133) over the fixed pair list
+ * s->pair_a/pair_b[0..n_pairs); overlap participants OR-ed into
+ * s->overlap_flags; with_tri: every sweep's crossings are applied to s->tri.
+ * result = {status (0 / BD_ERR_NONCONV), sweeps}.  The workspace must be
+ * sized with p->pair_capacity >= n_pairs. */
+int bd_overlap_correct(const bd_state_t* s, const bd_params_t* p, int64_t n_pairs, int with_tri,
+                       int64_t* result, void* stream);
+
+/* save_state / restore_state (triangulation.py:158-164): copy the six
+ * arrays of src into dst (same ne, nt) */
+int bd_tri_copy(const bd_tri_t* src, const bd_tri_t* dst, void* stream);
+
 /* clears the sticky error status of a state (after the host handled it) */
 int bd_clear_status(const bd_state_t* s, void* stream);
 

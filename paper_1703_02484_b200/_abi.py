@@ -87,6 +87,17 @@ def _protos():
         "bd_tri_restore_delaunay": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
         "bd_clear_status": ([P(BdState), c_vp], c_int),
         "bd_tri_audit_geometry": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
+        "bd_integrate": ([P(BdState), P(BdParams), c_d, c_vp, c_vp, c_vp], c_int),
+        "bd_tri_apply_crossings": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
+        "bd_tri_edge_inversion": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
+        "bd_tri_signed_area2": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
+        "bd_tri_delaunay_flags": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
+        "bd_tri_inverted_edge_flags": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
+        "bd_tri_flip_edges": ([P(BdState), P(BdParams), c_vp, c_i64, c_vp, c_vp], c_int),
+        "bd_tri_repair_inversions": ([P(BdState), P(BdParams), c_i64, c_int, c_vp, c_vp], c_int),
+        "bd_tri_restore_delaunay_ex": ([P(BdState), P(BdParams), c_i64, c_vp, c_vp], c_int),
+        "bd_overlap_correct": ([P(BdState), P(BdParams), c_i64, c_int, c_vp, c_vp], c_int),
+        "bd_tri_copy": ([P(BdTri), P(BdTri), c_vp], c_int),
         "bd_build_info": ([], ctypes.c_char_p),
     }
 
@@ -106,4 +117,7 @@ EXPORTS = ("bd_brute_overlaps", "bd_force","bd_force_prepare", "bd_force_slots",
            "bd_long_range_forces", "bd_short_range_forces", "bd_overlap_pass",
            "bd_max_sq_displacement", "bd_verlet_build", "bd_pairs_workspace_bytes", "bd_normals",
            "bd_step_tri", "bd_run_tri", "bd_step_verlet", "bd_run_verlet",
-           "bd_tri_restore_delaunay", "bd_clear_status", "bd_tri_audit_geometry", "bd_build_info")
+           "bd_tri_restore_delaunay", "bd_clear_status", "bd_tri_audit_geometry", "bd_build_info",
+           "bd_integrate", "bd_tri_apply_crossings", "bd_tri_edge_inversion", "bd_tri_signed_area2",
+           "bd_tri_delaunay_flags", "bd_tri_inverted_edge_flags", "bd_tri_flip_edges", "bd_tri_repair_inversions",
+           "bd_tri_restore_delaunay_ex", "bd_overlap_correct", "bd_tri_copy")

@@ -10,6 +10,7 @@
 
 #include "bd_allpairs.cuh"
 #include "bd_drivers.cuh"
+#include "bd_ops.cuh"
 
 using namespace bd;
 
@@ -81,6 +82,47 @@ __global__ void __launch_bounds__(STEP_BT) k_restore_delaunay_grid(bd_state_t s,
     Ctx c = make_ctx(s, p);
     ExecGrid x{c.w.ctl};
     restore_delaunay_entry(x, c, out);
+}
+
+// ---- method-boundary ops (bd_ops.cuh), one cooperative launch each --------
+enum : int64_t {
+    OP_INTEGRATE = 1, OP_APPLY_CROSSINGS, OP_EDGE_INVERSION, OP_SIGNED_AREA2, OP_DELAUNAY_FLAGS,
+    OP_INVERTED_FLAGS, OP_FLIP_EDGES, OP_REPAIR, OP_RESTORE, OP_CORRECT_OVERLAPS
+};
+
+struct OpArgs {
+    int64_t op, i0, i1;
+    double d0;
+    const void* in;
+    void* out;
+    int64_t* res;
+};
+
+__global__ void __launch_bounds__(STEP_BT) k_op_grid(bd_state_t s, bd_params_t p, OpArgs a) {
+    Ctx c = make_ctx(s, p);
+    ExecGrid x{c.w.ctl};
+    switch (a.op) {
+        case OP_INTEGRATE: op_integrate(x, c, a.d0, (int64_t*)a.out, a.res); break;
+        case OP_APPLY_CROSSINGS: op_apply_crossings(x, c, (const int64_t*)a.in); break;
+        case OP_EDGE_INVERSION: op_edge_inversion(x, c, a.res); break;
+        case OP_SIGNED_AREA2: op_signed_area2(x, c, (double*)a.out); break;
+        case OP_DELAUNAY_FLAGS: op_edge_flags(x, c, false, (uint8_t*)a.out); break;
+        case OP_INVERTED_FLAGS: op_edge_flags(x, c, true, (uint8_t*)a.out); break;
+        case OP_FLIP_EDGES: op_flip_edges(x, c, (const int64_t*)a.in, a.i0, a.res); break;
+        case OP_REPAIR: op_repair_inversions(x, c, a.i0, a.i1 != 0, a.res); break;
+        case OP_RESTORE: op_restore_delaunay(x, c, a.i0, a.res); break;
+        case OP_CORRECT_OVERLAPS: op_correct_overlaps(x, c, a.i0, a.i1 != 0, a.res); break;
+        default: break;
+    }
+}
+
+// save_state / restore_state (triangulation.py:158-164)
+__global__ void k_tri_copy(bd_tri_t a, bd_tri_t b) {
+    struct Flat {
+        BD_DEV int64_t tid() const { return blockIdx.x * (int64_t)blockDim.x + threadIdx.x; }
+        BD_DEV int64_t nth() const { return (int64_t)gridDim.x * blockDim.x; }
+    } x;
+    ph_tri_copy(x, a, b);
 }
 
 // ---- kernel-boundary drop-ins over pair lists (cooperative grid) ----------
@@ -255,7 +297,7 @@ void init_device_info() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         int m = occupancy((const void*)k_step_tri_grid, STEP_BT);
-        const void* coop[] = {(const void*)k_restore_delaunay_grid, (const void*)k_step_verlet_grid,
+        const void* coop[] = {(const void*)k_restore_delaunay_grid, (const void*)k_op_grid, (const void*)k_step_verlet_grid,
                               (const void*)k_verlet_build_grid, (const void*)k_short_range_grid,
                               (const void*)k_overlap_pass_grid};
         for (const void* f : coop) {
@@ -398,6 +440,15 @@ int launch_step_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, 
 
 int launch_step_verlet(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
     return launch_driver((const void*)k_step_verlet_grid, (const void*)k_step_verlet_block, s, p, out, st);
+}
+
+int launch_op(const bd_state_t* s, const bd_params_t* p, OpArgs a, int64_t items, cudaStream_t st) {
+    init_device_info();
+    bd_state_t sv = *s;
+    bd_params_t pv = *p;
+    void* args[] = {&sv, &pv, &a};
+    if (items < p->n) items = p->n;
+    return coop_launch((const void*)k_op_grid, items, args, st);
 }
 
 // a transient state for the standalone pair-list entry points
@@ -634,6 +685,66 @@ int bd_tri_restore_delaunay(const bd_state_t* s, const bd_params_t* p, int64_t* 
     void* args[] = {&sv, &pv, &passes_out};
     const int64_t items = s->tri.ne > p->n ? s->tri.ne : p->n;
     return coop_launch((const void*)k_restore_delaunay_grid, items, args, (cudaStream_t)stream);
+}
+
+int bd_integrate(const bd_state_t* s, const bd_params_t* p, double dt, int64_t* crossings, int64_t* result,
+                 void* stream) {
+    return launch_op(s, p, OpArgs{OP_INTEGRATE, 0, 0, dt, nullptr, crossings, result}, p->n, (cudaStream_t)stream);
+}
+
+int bd_tri_apply_crossings(const bd_state_t* s, const bd_params_t* p, const int64_t* crossings, void* stream) {
+    return launch_op(s, p, OpArgs{OP_APPLY_CROSSINGS, 0, 0, 0.0, crossings, nullptr, nullptr}, s->tri.nt,
+                     (cudaStream_t)stream);
+}
+
+int bd_tri_edge_inversion(const bd_state_t* s, const bd_params_t* p, int64_t* result, void* stream) {
+    return launch_op(s, p, OpArgs{OP_EDGE_INVERSION, 0, 0, 0.0, nullptr, nullptr, result}, s->tri.ne,
+                     (cudaStream_t)stream);
+}
+
+int bd_tri_signed_area2(const bd_state_t* s, const bd_params_t* p, double* area, void* stream) {
+    return launch_op(s, p, OpArgs{OP_SIGNED_AREA2, 0, 0, 0.0, nullptr, area, nullptr}, s->tri.nt,
+                     (cudaStream_t)stream);
+}
+
+int bd_tri_delaunay_flags(const bd_state_t* s, const bd_params_t* p, uint8_t* flags, void* stream) {
+    return launch_op(s, p, OpArgs{OP_DELAUNAY_FLAGS, 0, 0, 0.0, nullptr, flags, nullptr}, s->tri.ne,
+                     (cudaStream_t)stream);
+}
+
+int bd_tri_inverted_edge_flags(const bd_state_t* s, const bd_params_t* p, uint8_t* flags, void* stream) {
+    return launch_op(s, p, OpArgs{OP_INVERTED_FLAGS, 0, 0, 0.0, nullptr, flags, nullptr}, s->tri.ne,
+                     (cudaStream_t)stream);
+}
+
+int bd_tri_flip_edges(const bd_state_t* s, const bd_params_t* p, const int64_t* edges, int64_t count,
+                      int64_t* result, void* stream) {
+    return launch_op(s, p, OpArgs{OP_FLIP_EDGES, count, 0, 0.0, edges, nullptr, result}, 1, (cudaStream_t)stream);
+}
+
+int bd_tri_repair_inversions(const bd_state_t* s, const bd_params_t* p, int64_t max_passes, int use_prev,
+                             int64_t* result, void* stream) {
+    return launch_op(s, p, OpArgs{OP_REPAIR, max_passes, use_prev, 0.0, nullptr, nullptr, result}, s->tri.ne,
+                     (cudaStream_t)stream);
+}
+
+int bd_tri_restore_delaunay_ex(const bd_state_t* s, const bd_params_t* p, int64_t max_passes, int64_t* result,
+                               void* stream) {
+    return launch_op(s, p, OpArgs{OP_RESTORE, max_passes, 0, 0.0, nullptr, nullptr, result}, s->tri.ne,
+                     (cudaStream_t)stream);
+}
+
+int bd_overlap_correct(const bd_state_t* s, const bd_params_t* p, int64_t n_pairs, int with_tri, int64_t* result,
+                       void* stream) {
+    return launch_op(s, p, OpArgs{OP_CORRECT_OVERLAPS, n_pairs, with_tri, 0.0, nullptr, nullptr, result}, n_pairs,
+                     (cudaStream_t)stream);
+}
+
+int bd_tri_copy(const bd_tri_t* src, const bd_tri_t* dst, void* stream) {
+    init_device_info();
+    const int64_t items = src->ne > src->nt ? src->ne : src->nt;
+    k_tri_copy<<<grid_for(items), 256, 0, (cudaStream_t)stream>>>(*src, *dst);
+    return err_code(cudaGetLastError());
 }
 
 int bd_tri_audit_geometry(const bd_state_t* s, const bd_params_t* p, int64_t* out, void* stream) {

@@ -249,7 +249,7 @@ BD_HD void ph_tri_copy(X& x, const bd_tri_t& a, bd_tri_t& b) {
 
 // integrate (dynamics.py:73-94) fused with the crossing bookkeeping; returns #particles that crossed
 template <class X>
-BD_HD u64 ph_integrate(X& x, Red<X>& R, Ctx& c, double dt) {
+BD_HD u64 ph_integrate(X& x, Red<X>& R, Ctx& c, double dt, int64_t* cross64 = nullptr) {
     u64* r = R.open();
     const double L = c.p.L, scale = sqrt(c.p.diffusion * dt), clamp = c.p.clamp;
     double* pos = c.s.pos;
@@ -266,6 +266,7 @@ BD_HD u64 ph_integrate(X& x, Red<X>& R, Ctx& c, double dt) {
             const long long ci = (long long)rint((nw - w) / L);
             pos[2 * i + k] = w;
             c.w.cross8[2 * i + k] = (int8_t)ci;
+            if (cross64) cross64[2 * i + k] = (int64_t)ci;
             if (c.s.image) c.s.image[2 * i + k] += (int32_t)ci;
             crossed |= ci != 0;
         }
@@ -407,18 +408,22 @@ BD_HD int64_t restore_delaunay(X& x, Red<X>& R, Ctx& c, int64_t max_passes) {
     }
 }
 
-// repair_inversions (triangulation.py:336-363) with prev = positions_prev.
-// returns 0 ok, 1 needs rollback, -1 error; adds flips to *flips
+// repair_inversions (triangulation.py:336-363) with prev = positions_prev
+// (use_prev = false: the reference's prev=None, local predicate only).
+// returns 0 ok, 1 needs rollback, -1 error; adds flips to *flips and, if
+// given, the reference's RepairResult.passes to *passes
 template <class X>
-BD_HD int repair_inversions(X& x, Red<X>& R, Ctx& c, int64_t max_passes, int64_t* flips) {
+BD_HD int repair_inversions(X& x, Red<X>& R, Ctx& c, int64_t max_passes, int64_t* flips, bool use_prev = true,
+                            int64_t* passes = nullptr) {
     bd_tri_t& T = c.s.tri;
     for (int64_t pass = 0; pass < max_passes; ++pass) {
+        if (passes) *passes = pass;
         if (ph_inverted_tris(x, R, c) == 0) return 0;
         for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
             V2 q[4];
             edge_quad(T, c.s.pos, c.p.L, e, q);
             bool f = point_in_tri(q[3], q[0], q[1], q[2]) | point_in_tri(q[2], q[0], q[1], q[3]);
-            for (int side = 0; side < 2 && !f; ++side) {
+            for (int side = 0; side < 2 && !f && use_prev; ++side) {
                 const int64_t t = T.edge_tri[2 * e + side];
                 if (c.w.tinv[t]) f = crossed_side(T, c.s.pos, c.s.prev, c.p, t, T.edge_opp[2 * e + side]);
             }
@@ -430,6 +435,7 @@ BD_HD int repair_inversions(X& x, Red<X>& R, Ctx& c, int64_t max_passes, int64_t
         if (chosen == 0) return 1;
         *flips += (int64_t)chosen;
     }
+    if (passes) *passes = max_passes;
     return ph_inverted_tris(x, R, c) != 0 ? 1 : 0;
 }
 

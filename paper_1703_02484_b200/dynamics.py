@@ -134,6 +134,67 @@ class _Engine:
         check(lib().bd_clear_status(ctypes.byref(self.s), _stream()), "bd_clear_status")
 
 
+def _rng_counter(rng):
+    for k in ("seed", "stream", "call"):
+        if not hasattr(rng, k):
+            raise BrownsimError("the device noise is counter-based: rng must be a CounterRng (seed, stream, call)")
+    return int(rng.seed) & ((1 << 64) - 1), int(rng.stream) & ((1 << 64) - 1), int(rng.call)
+
+
+def integrate(sys: ParticleSystem, forces, params: SimParams, rng, dt: float | None = None) -> np.ndarray:
+    """dynamics.py:73-94 on the GPU: one Euler-Maruyama update of all
+    positions (prev <- pos; pos = wrap((pos + F dt) + xi sqrt(D dt)), xi the
+    clamped counter normals of call rng.call, which advances by one);
+    returns the box crossings (N, 2) int64.  Non-finite forces raise
+    StepFailure before anything moves."""
+    import torch
+    from ._ops import OpState, as_device
+    if dt is None:
+        dt = params.dt
+    seed, stream, call = _rng_counter(rng)
+    n = sys.n
+    f = as_device(forces, torch.float64, sys.device, (n, 2))
+    op = OpState(n, sys.box.length, sys.device)
+    op.p.diffusion, op.p.clamp, op.p.sigma = float(params.diffusion), float(params.noise_clamp), float(params.sigma)
+    op.p.seed, op.p.stream = seed, stream
+    op.call_t.fill_(call)
+    cross = torch.zeros((n, 2), dtype=torch.int64, device=sys.device)
+    op.bind(pos=sys.positions_t, prev=sys.positions_prev_t, force=f, image=sys.image_t)
+    res = op.run("bd_integrate", ctypes.c_double(float(dt)), ctypes.c_void_p(cross.data_ptr()), op.res_ptr)
+    if res[0] == _abi.BD_ERR_STEPFAIL:
+        raise StepFailure(f"non-finite force on particle {int(res[2])}")
+    rng.call = call + 1
+    return cross.cpu().numpy()
+
+
+def correct_overlaps(sys: ParticleSystem, pair_a, pair_b, params: SimParams, tri: PeriodicTriangulation | None = None,
+                     flags_out: np.ndarray | None = None) -> int:
+    """dynamics.py:97-133 on the GPU: push overlapping pairs of the fixed
+    list apart (per-particle sums in ascending pair order, displacement
+    capped at params.displacement_cap, wrap) until none remain; with `tri`
+    every sweep's crossings are applied to it.  Returns the sweeps that
+    corrected something; NonConvergenceError after max_overlap_iters."""
+    import torch
+    from ._ops import OpState, as_device
+    pa = as_device(pair_a, torch.int64, sys.device).reshape(-1)
+    pb = as_device(pair_b, torch.int64, sys.device).reshape(-1)
+    m = int(pa.numel())
+    n = sys.n
+    op = OpState(n, sys.box.length, sys.device, tri=tri, n_pairs=max(m, 1), sigma=params.sigma)
+    op.p.cap = float(params.displacement_cap)
+    op.p.max_overlap_iters = int(params.max_overlap_iters)
+    flags = torch.zeros(n, dtype=torch.uint8, device=sys.device)
+    op.bind(pos=sys.positions_t, pair_a=pa, pair_b=pb, overlap_flags=flags, image=sys.image_t)
+    res = op.run("bd_overlap_correct", m, int(tri is not None), op.res_ptr)
+    if flags_out is not None:
+        flags_out |= flags.cpu().numpy().astype(bool)
+    if res[0] == _abi.BD_ERR_NONCONV:
+        raise NonConvergenceError(f"overlap correction still unresolved after {params.max_overlap_iters} sweeps")
+    if res[0]:
+        raise BrownsimError(f"correct_overlaps: device status {int(res[0])}")
+    return int(res[1])
+
+
 def _raise_for(st: dict, step_index: int):
     code = int(st["status"])
     if code == _abi.BD_OK:

@@ -15,11 +15,12 @@ The post-build Delaunay clean-up pass runs on the GPU.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from .core import BuildError, PeriodicBox
+from .core import BrownsimError, BuildError, NonConvergenceError, PeriodicBox
 
 DEFAULT_TOL = 1e-12
 _JITTER_KEY = (0x7C94_1EAF, 0x0B5E_55ED)  # triangulation.py:24 (build jitter must match)
@@ -28,6 +29,23 @@ _DTYPES = {"tri_v": np.int32, "tri_shift": np.int8, "tri_edge": np.int32, "edge_
            "edge_tri": np.int32, "edge_opp": np.int8}
 _SHAPES = {"tri_v": (3,), "tri_shift": (3, 2), "tri_edge": (3,), "edge_v": (2,), "edge_tri": (2,),
            "edge_opp": (2,)}
+
+
+@dataclass(frozen=True)
+class FlipDecision:
+    """triangulation.py:27-30"""
+
+    edge: int
+    reason: str  # "delaunay-violation" | "inverted-triangle"
+
+
+@dataclass
+class RepairResult:
+    """triangulation.py:33-37"""
+
+    flips: int
+    passes: int
+    needs_rollback: bool
 
 
 @dataclass
@@ -117,17 +135,104 @@ class PeriodicTriangulation:
         for k in TRI_KEYS:
             self._t[k].copy_(state[k])
 
+    # -- device methods (the reference's method boundary, csrc/bd_ops.cuh) --
+    # Each runs one cooperative launch on this triangulation's device arrays
+    # and the given positions (numpy or CUDA tensors), then returns host
+    # values like the reference's numpy methods do.
+
+    def _ops(self, n_pairs: int = 0):
+        from ._ops import OpState
+        return OpState(self.n_vertices, self.box.length, self.device, tri=self, n_pairs=n_pairs, tol=self.tol)
+
+    def _pos(self, positions):
+        import torch
+        from ._ops import as_device
+        return as_device(positions, torch.float64, self.device, (self.n_vertices, 2))
+
+    def apply_crossings(self, crossings):
+        """triangulation.py:166-177 (device)."""
+        import torch
+        from ._ops import as_device
+        cr = as_device(crossings, torch.int64, self.device, (self.n_vertices, 2))
+        op = self._ops()
+        op.run("bd_tri_apply_crossings", ctypes.c_void_p(cr.data_ptr()))
+
+    def signed_area2(self, positions) -> np.ndarray:
+        """triangulation.py:186-191 (device): twice the signed area per triangle."""
+        import torch
+        out = torch.empty(self.n_triangles, dtype=torch.float64, device=self.device)
+        op = self._ops().bind(pos=self._pos(positions))
+        op.run("bd_tri_signed_area2", ctypes.c_void_p(out.data_ptr()))
+        return out.cpu().numpy()
+
+    def _edge_flags(self, name, positions, tol=None) -> np.ndarray:
+        import torch
+        out = torch.empty(self.n_edges, dtype=torch.uint8, device=self.device)
+        op = self._ops().bind(pos=self._pos(positions))
+        if tol is not None:
+            op.p.tol = float(tol)
+        op.run(name, ctypes.c_void_p(out.data_ptr()))
+        return out.cpu().numpy().astype(bool)
+
+    def delaunay_flags(self, positions, tol: float | None = None) -> np.ndarray:
+        """triangulation.py:226-229 (device): right opposite vertex inside the left circumcircle."""
+        return self._edge_flags("bd_tri_delaunay_flags", positions, tol)
+
+    def inverted_edge_flags(self, positions) -> np.ndarray:
+        """triangulation.py:231-234 (device): point-in-triangle inversion predicate."""
+        return self._edge_flags("bd_tri_inverted_edge_flags", positions)
+
+    def detect_inverted_triangles(self, positions) -> list:
+        """triangulation.py:236-238"""
+        flags = self.inverted_edge_flags(positions)
+        return [FlipDecision(int(e), "inverted-triangle") for e in np.flatnonzero(flags)]
+
+    def edge_inversion_present(self, prev, curr) -> bool:
+        """triangulation.py:240-250 (device): some edge vector reversed its sign."""
+        op = self._ops().bind(pos=self._pos(curr), prev=self._pos(prev))
+        return bool(op.run("bd_tri_edge_inversion", op.res_ptr)[0])
+
+    def flip_edge(self, e: int):
+        """triangulation.py:254-302 (device): replace edge (a, b) by the cross diagonal (c, d)."""
+        self.flip_edges([int(e)])
+
+    def flip_edges(self, edges):
+        """flip_edge for each edge in order (one launch)."""
+        import torch
+        ed = torch.as_tensor(np.asarray(edges, dtype=np.int64).reshape(-1)).to(self.device)
+        op = self._ops()
+        res = op.run("bd_tri_flip_edges", ctypes.c_void_p(ed.data_ptr()), int(ed.numel()), op.res_ptr)
+        if res[0]:
+            raise BrownsimError(f"edge {int(ed[int(res[1])])} cannot be flipped (degenerate or glued quad)")
+
+    def restore_delaunay(self, positions, tol: float | None = None, max_passes: int = 1000) -> int:
+        """triangulation.py:319-334 (device): Lawson flips in greedy
+        ascending-edge independent sets until no in-circle violation; passes."""
+        op = self._ops().bind(pos=self._pos(positions))
+        if tol is not None:
+            op.p.tol = float(tol)
+        res = op.run("bd_tri_restore_delaunay_ex", int(max_passes), op.res_ptr)
+        if res[0] == 2:
+            raise NonConvergenceError(f"delaunay restoration did not converge in {max_passes} passes")
+        if res[0]:
+            raise BrownsimError(f"restore_delaunay: edge {int(res[1])} cannot be flipped")
+        return int(res[1])
+
+    def repair_inversions(self, positions, prev=None, max_passes: int = 10) -> RepairResult:
+        """triangulation.py:336-363 (device): flip away inverted triangles;
+        with `prev`, edges crossed by a vertex's path are flagged too."""
+        pos = self._pos(positions)
+        op = self._ops().bind(pos=pos, prev=self._pos(prev) if prev is not None else pos)
+        res = op.run("bd_tri_repair_inversions", int(max_passes), int(prev is not None), op.res_ptr)
+        if res[0]:
+            raise BrownsimError(f"repair_inversions: device status {int(res[0])}")
+        return RepairResult(int(res[1]), int(res[2]), bool(res[3]))
+
     # -- host-side geometry (validation / read-out only) --------------------
 
     def tri_coords(self, positions) -> np.ndarray:
         pos = np.asarray(positions, dtype=np.float64)
         return pos[self.tri_v] + self.tri_shift.astype(np.float64) * self.box.length
-
-    def signed_area2(self, positions) -> np.ndarray:
-        xy = self.tri_coords(positions)
-        e1 = xy[:, 1] - xy[:, 0]
-        e2 = xy[:, 2] - xy[:, 0]
-        return e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0]
 
     def edge_quads(self, positions):
         return host_edge_quads(self.arrays(), positions, self.box.length)

@@ -9,6 +9,7 @@
 // uses it.
 #include "../../paper_1703_02484_b200/csrc/bd_allpairs.cuh"
 #include "../../paper_1703_02484_b200/csrc/bd_drivers.cuh"
+#include "../../paper_1703_02484_b200/csrc/bd_ops.cuh"
 
 using namespace bd;
 
@@ -77,6 +78,26 @@ int64_t bdh_verlet_build(const bd_state_t* s, const bd_params_t* p, double margi
     c.w.ctl->status = 0;
     if (!vl_rebuild(x, R, c, margin)) return -1;
     return c.s.vl_meta[0];
+}
+
+// the method-boundary ops of csrc/bd_ops.cuh (op codes as in bd_capi.cu)
+void bdh_op(const bd_state_t* s, const bd_params_t* p, int64_t op, int64_t i0, int64_t i1, double d0, const void* in,
+            void* out, int64_t* res) {
+    Ctx c = host_ctx(s, p);
+    ExecHost x{c.w.ctl};
+    switch (op) {
+        case 1: op_integrate(x, c, d0, (int64_t*)out, res); break;
+        case 2: op_apply_crossings(x, c, (const int64_t*)in); break;
+        case 3: op_edge_inversion(x, c, res); break;
+        case 4: op_signed_area2(x, c, (double*)out); break;
+        case 5: op_edge_flags(x, c, false, (uint8_t*)out); break;
+        case 6: op_edge_flags(x, c, true, (uint8_t*)out); break;
+        case 7: op_flip_edges(x, c, (const int64_t*)in, i0, res); break;
+        case 8: op_repair_inversions(x, c, i0, i1 != 0, res); break;
+        case 9: op_restore_delaunay(x, c, i0, res); break;
+        case 10: op_correct_overlaps(x, c, i0, i1 != 0, res); break;
+        default: break;
+    }
 }
 
 }  // extern "C"
