@@ -74,6 +74,10 @@ typedef struct bd_params {
     double r_list;        /* Verlet list radius max(r_cut, sigma) + skin */
     int64_t ncx;          /* cells per axis of the Verlet grid (0 = all-pairs scan) */
     int64_t pair_capacity;/* capacity of the Verlet pair buffers */
+    /* active Brownian particles (AbpState, dynamics.py:60-66, :349-399) */
+    double abp_speed;         /* self-propulsion speed V0 */
+    double abp_rot_diffusion; /* rotational diffusion D_r */
+    int64_t abp_clamp_angle;  /* clamp the angular noise (clamp_angle_noise) */
 } bd_params_t;
 
 /* StepStats (dynamics.py:42-57) counters + error report */
@@ -102,6 +106,7 @@ typedef struct bd_state {
     int64_t* vl_meta; /* [0]=n_pairs, [1]=valid, [2]=rebuilds total, [3]=overlap candidates */
     void* work;       /* scratch of bd_workspace_bytes() bytes */
     int64_t work_bytes;
+    double* angles;   /* (n,) ABP director angles (AbpState.angles), else NULL */
 } bd_state_t;
 
 /* fills p->mi_lo/mi_hi (and r_list/ncx) from p->L etc.; host-only helper */
@@ -202,6 +207,15 @@ int bd_step_verlet(const bd_state_t* s, const bd_params_t* p, bd_stats_t* stats_
 /* `steps` consecutive ShortRangeSimulation steps (stats_out[j], device) */
 int bd_run_verlet(const bd_state_t* s, const bd_params_t* p, int64_t steps, bd_stats_t* stats_out,
                   void* stream);
+
+/* one AbpSimulation.step (dynamics.py:368-399): Verlet list kept fresh,
+ * ballistic move by V0 dt (cos theta, sin theta), angles += sqrt(2 D_r dt) xi
+ * (xi = counter normals of one call, clamped if p->abp_clamp_angle), overlap
+ * rounds over the candidates within sigma + skin -- one persistent kernel */
+int bd_step_abp(const bd_state_t* s, const bd_params_t* p, bd_stats_t* stats_out, void* stream);
+
+/* `steps` consecutive AbpSimulation steps (stats_out[j], device) */
+int bd_run_abp(const bd_state_t* s, const bd_params_t* p, int64_t steps, bd_stats_t* stats_out, void* stream);
 
 /* restore_delaunay (triangulation.py:319-334) on the state's triangulation
  * and positions; passes (or -1 on error) written to passes_out[0] (device) */

@@ -9,7 +9,8 @@ import this module; the product package never does.
   mode "tri"    -> LongRangeSimulation.step (dynamics.py:191-274) with the
                    force model force_mode 0 (long range), 1 (short range over
                    a Verlet list), 2 (long + short), SURVEY.md §0 composites;
-  mode "verlet" -> ShortRangeSimulation.step (dynamics.py:326-346).
+  mode "verlet" -> ShortRangeSimulation.step (dynamics.py:326-346);
+  mode "abp"    -> AbpSimulation.step (dynamics.py:368-399), see set_abp().
 """
 
 from __future__ import annotations
@@ -107,6 +108,8 @@ def _declare(L):
     L.bdo_sim_step_tri.restype = ctypes.c_int
     L.bdo_sim_step_verlet.argtypes = [vp, vp, d]
     L.bdo_sim_step_verlet.restype = ctypes.c_int
+    L.bdo_sim_step_abp.argtypes = [vp, vp, vp, d, d, ctypes.c_int, d]
+    L.bdo_sim_step_abp.restype = ctypes.c_int
     L.bdo_sim_alloc_scratch.argtypes = [vp]
     L.bdo_sim_free_scratch.argtypes = [vp]
     L.bdo_sim_struct_size.restype = i64
@@ -355,9 +358,24 @@ class OracleSim:
     def rebuilds(self):
         return self._s.rebuilds
 
+    def set_abp(self, angles, speed, rot_diffusion, clamp_angle=False, skin=None):
+        """mode "abp": AbpSimulation.step (dynamics.py:349-399); r_list =
+        overlap_margin = sigma + skin."""
+        self.mode = "abp"
+        self.angles = np.ascontiguousarray(angles, np.float64).copy()
+        self.abp = (float(speed), float(rot_diffusion), int(bool(clamp_angle)))
+        self.r_list = self._s.sigma + self.skin
+        self.overlap_margin = self.r_list
+        self._s.r_list = self.r_list
+        self._s.r_cut = 0.0
+        return self
+
     def step(self) -> dict:
         st = StatsStruct()
-        if self.mode == "tri":
+        if self.mode == "abp":
+            lib().bdo_sim_step_abp(ctypes.byref(self._s), ctypes.byref(st), _p(self.angles), *self.abp,
+                                   self.overlap_margin)
+        elif self.mode == "tri":
             lib().bdo_sim_step_tri(ctypes.byref(self._s), ctypes.byref(st))
         else:
             lib().bdo_sim_step_verlet(ctypes.byref(self._s), ctypes.byref(st), self.overlap_margin)

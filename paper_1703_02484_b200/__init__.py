@@ -17,10 +17,12 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # GPU-side modules load lazily so that `import paper_1703_02484_b200` works
     # on a CPU-only host for setup / build tooling
-    if name in ("LongRangeSimulation", "StepStats", "MissedOverlapError"):
+    if name in ("LongRangeSimulation", "ShortRangeSimulation", "AbpSimulation", "AbpState", "StepStats",
+                "MissedOverlapError", "integrate", "correct_overlaps"):
         from . import dynamics
         return getattr(dynamics, name)
-    if name in ("PeriodicTriangulation", "build_initial", "incircle", "AuditReport"):
+    if name in ("PeriodicTriangulation", "build_initial", "incircle", "AuditReport", "RepairResult",
+                "FlipDecision"):
         from . import triangulation
         return getattr(triangulation, name)
     raise AttributeError(name)

@@ -35,7 +35,8 @@ class BdParams(ctypes.Structure):
                 ("seed", c_u64), ("stream", c_u64),
                 ("force_mode", c_i64), ("lr_precision", c_i64),
                 ("mi_lo", c_d), ("mi_hi", c_d), ("r_list", c_d), ("ncx", c_i64),
-                ("pair_capacity", c_i64)]
+                ("pair_capacity", c_i64),
+                ("abp_speed", c_d), ("abp_rot_diffusion", c_d), ("abp_clamp_angle", c_i64)]
 
 
 class BdStats(ctypes.Structure):
@@ -53,7 +54,7 @@ class BdState(ctypes.Structure):
                 ("force_err", c_vp), ("image", c_vp), ("overlap_flags", c_vp),
                 ("tri", BdTri), ("tri_backup", BdTri), ("call", c_vp), ("stats", c_vp),
                 ("pair_a", c_vp), ("pair_b", c_vp), ("vl_snap", c_vp), ("vl_meta", c_vp),
-                ("work", c_vp), ("work_bytes", c_i64)]
+                ("work", c_vp), ("work_bytes", c_i64), ("angles", c_vp)]
 
 
 _PROTOS = None
@@ -84,6 +85,8 @@ def _protos():
         "bd_run_tri": ([P(BdState), P(BdParams), c_i64, c_vp, c_vp], c_int),
         "bd_step_verlet": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
         "bd_run_verlet": ([P(BdState), P(BdParams), c_i64, c_vp, c_vp], c_int),
+        "bd_step_abp": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
+        "bd_run_abp": ([P(BdState), P(BdParams), c_i64, c_vp, c_vp], c_int),
         "bd_tri_restore_delaunay": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
         "bd_clear_status": ([P(BdState), c_vp], c_int),
         "bd_tri_audit_geometry": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
@@ -120,4 +123,4 @@ EXPORTS = ("bd_brute_overlaps", "bd_force","bd_force_prepare", "bd_force_slots",
            "bd_tri_restore_delaunay", "bd_clear_status", "bd_tri_audit_geometry", "bd_build_info",
            "bd_integrate", "bd_tri_apply_crossings", "bd_tri_edge_inversion", "bd_tri_signed_area2",
            "bd_tri_delaunay_flags", "bd_tri_inverted_edge_flags", "bd_tri_flip_edges", "bd_tri_repair_inversions",
-           "bd_tri_restore_delaunay_ex", "bd_overlap_correct", "bd_tri_copy")
+           "bd_tri_restore_delaunay_ex", "bd_overlap_correct", "bd_tri_copy", "bd_step_abp", "bd_run_abp")

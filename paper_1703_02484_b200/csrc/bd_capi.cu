@@ -68,6 +68,18 @@ __global__ void __launch_bounds__(BLOCK_BT) k_step_verlet_block(bd_state_t s, bd
     step_verlet(x, c, out);
 }
 
+__global__ void __launch_bounds__(STEP_BT) k_step_abp_grid(bd_state_t s, bd_params_t p, bd_stats_t* out) {
+    Ctx c = make_ctx(s, p);
+    ExecGrid x{c.w.ctl};
+    step_abp(x, c, out);
+}
+
+__global__ void __launch_bounds__(BLOCK_BT) k_step_abp_block(bd_state_t s, bd_params_t p, bd_stats_t* out) {
+    Ctx c = make_ctx(s, p);
+    ExecBlock x{c.w.ctl};
+    step_abp(x, c, out);
+}
+
 template <class X>
 __device__ void restore_delaunay_entry(X& x, Ctx& c, int64_t* passes_out) {
     Red<X> R(x);
@@ -297,7 +309,7 @@ void init_device_info() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         int m = occupancy((const void*)k_step_tri_grid, STEP_BT);
-        const void* coop[] = {(const void*)k_restore_delaunay_grid, (const void*)k_op_grid, (const void*)k_step_verlet_grid,
+        const void* coop[] = {(const void*)k_restore_delaunay_grid, (const void*)k_op_grid, (const void*)k_step_abp_grid, (const void*)k_step_verlet_grid,
                               (const void*)k_verlet_build_grid, (const void*)k_short_range_grid,
                               (const void*)k_overlap_pass_grid};
         for (const void* f : coop) {
@@ -449,6 +461,10 @@ int launch_op(const bd_state_t* s, const bd_params_t* p, OpArgs a, int64_t items
     void* args[] = {&sv, &pv, &a};
     if (items < p->n) items = p->n;
     return coop_launch((const void*)k_op_grid, items, args, st);
+}
+
+int launch_step_abp(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
+    return launch_driver((const void*)k_step_abp_grid, (const void*)k_step_abp_block, s, p, out, st);
 }
 
 // a transient state for the standalone pair-list entry points
@@ -668,6 +684,18 @@ int bd_step_verlet(const bd_state_t* s, const bd_params_t* p, bd_stats_t* stats_
 int bd_run_verlet(const bd_state_t* s, const bd_params_t* p, int64_t steps, bd_stats_t* stats_out, void* stream) {
     for (int64_t j = 0; j < steps; ++j) {
         int rc = launch_step_verlet(s, p, stats_out + j, (cudaStream_t)stream);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+int bd_step_abp(const bd_state_t* s, const bd_params_t* p, bd_stats_t* stats_out, void* stream) {
+    return launch_step_abp(s, p, stats_out, (cudaStream_t)stream);
+}
+
+int bd_run_abp(const bd_state_t* s, const bd_params_t* p, int64_t steps, bd_stats_t* stats_out, void* stream) {
+    for (int64_t j = 0; j < steps; ++j) {
+        int rc = launch_step_abp(s, p, stats_out + j, (cudaStream_t)stream);
         if (rc) return rc;
     }
     return 0;

@@ -168,6 +168,48 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
 }
 
 
+// _VerletNeighborMixin._overlap_rounds (dynamics.py:290-304): correct over
+// the overlap candidates; rebuild (candidates within `margin`) and repeat
+// while the motion since the snapshot exceeds skin/2.  Returns the sweeps.
+template <class X>
+BD_HD int64_t overlap_rounds(X& x, Red<X>& R, Ctx& c, double margin) {
+    int64_t iters = 0, round;
+    for (round = 0; round < c.p.max_overlap_iters; ++round) {
+        const SubsetPairs sp{c.s.pair_a, c.s.pair_b, c.w.ov_idx, (int64_t)x.ld((const u64*)&c.s.vl_meta[3])};
+        build_incidence(x, c.p.n, sp, c.w.inc_off, c.w.inc_cur, c.w.inc);
+        const int64_t ri = correct_overlaps(x, R, c, sp, false);
+        if (ri < 0) break;
+        iters += ri;
+        if (!vl_stale(x, R, c)) break;
+        if (!vl_rebuild(x, R, c, margin)) break;
+    }
+    if (!x.ld(&c.w.ctl->status) && round == c.p.max_overlap_iters) {
+        set_error(x, c, BD_ERR_NONCONV, 0, 0);
+        x.sync();
+    }
+    return iters;
+}
+
+template <class X>
+BD_HD void verlet_stats(X& x, Red<X>& R, Ctx& c, bd_stats_t* out, int64_t rebuilds0, int64_t iters) {
+    u64* r = R.open();
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) x.add(r, (u64)c.s.overlap_flags[i]);
+    const u64 nov = R.close(r);
+    if (x.leader()) {
+        out->rebuilds = c.s.vl_meta[2] - rebuilds0;
+        out->dt_used = c.p.dt;
+        out->overlap_iterations = iters;
+        out->flip_passes = 0;
+        out->inversion_repairs = 0;
+        out->rollbacks = 0;
+        out->n_overlapping = (int64_t)nov;
+        out->status = (int64_t)c.w.ctl->status;
+        out->err_i = (int64_t)c.w.ctl->err_i;
+        out->err_k = (int64_t)c.w.ctl->err_k;
+        *c.s.call = c.call;
+    }
+}
+
 // ShortRangeSimulation.step (dynamics.py:326-346): fresh list, short-range
 // force, integrate, overlap rounds over the overlap candidates with list
 // rebuilds whenever motion since the snapshot exceeds skin/2.
@@ -187,36 +229,62 @@ BD_HD void step_verlet(X& x, Ctx& c, bd_stats_t* out) {
     ph_integrate(x, R, c, c.p.dt);
     c.call++;
     for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) c.s.overlap_flags[i] = 0;
-    int64_t iters = 0, round;
-    for (round = 0; round < c.p.max_overlap_iters; ++round) {
-        const SubsetPairs sp{c.s.pair_a, c.s.pair_b, c.w.ov_idx, (int64_t)x.ld((const u64*)&c.s.vl_meta[3])};
-        build_incidence(x, c.p.n, sp, c.w.inc_off, c.w.inc_cur, c.w.inc);
-        const int64_t ri = correct_overlaps(x, R, c, sp, false);
-        if (ri < 0) break;
-        iters += ri;
-        if (!vl_stale(x, R, c)) break;
-        if (!vl_rebuild(x, R, c, margin)) break;
+    const int64_t iters = overlap_rounds(x, R, c, margin);
+    verlet_stats(x, R, c, out, rebuilds0, iters);
+}
+
+// AbpSimulation.step move (dynamics.py:378-390): prev <- pos; pos =
+// wrap(pos + (V0 dt) (cos theta, sin theta)); theta += sqrt(2 D_r dt) xi with
+// xi element i of one normals(n) call (pair i/2, component i%2), clamped
+// when clamp_angle_noise.  Crossings feed the image counters (MSD).
+template <class X>
+BD_HD void ph_abp_move(X& x, Ctx& c) {
+    const double L = c.p.L, s = c.p.abp_speed * c.p.dt;
+    const double ang_scale = sqrt(2.0 * c.p.abp_rot_diffusion * c.p.dt);
+    double* pos = c.s.pos;
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
+        const double th = c.s.angles[i];
+        double h[2];
+#if defined(__CUDA_ARCH__)
+        sincos(th, &h[1], &h[0]);
+#else
+        h[0] = cos(th);
+        h[1] = sin(th);
+#endif
+        for (int k = 0; k < 2; ++k) {
+            const double p0 = pos[2 * i + k];
+            c.s.prev[2 * i + k] = p0;
+            const double nw = p0 + s * h[k];
+            const double w = wrap1(nw, L);
+            pos[2 * i + k] = w;
+            if (c.s.image) c.s.image[2 * i + k] += (int32_t)rint((nw - w) / L);
+        }
+        double z0, z1;
+        normal_pair(c.p.seed, c.p.stream, c.call, (uint64_t)(i >> 1), 0, z0, z1);
+        double z = (i & 1) ? z1 : z0;
+        if (c.p.abp_clamp_angle) z = clampd(z, c.p.clamp);
+        c.s.angles[i] = th + ang_scale * z;
     }
-    if (!x.ld(&c.w.ctl->status) && round == c.p.max_overlap_iters) {
-        set_error(x, c, BD_ERR_NONCONV, 0, 0);
-        x.sync();
+    x.sync();
+}
+
+// AbpSimulation.step (dynamics.py:368-399): fresh list, ballistic move +
+// angle diffusion, overlap rounds with candidates within sigma + skin.
+template <class X>
+BD_HD void step_abp(X& x, Ctx& c, bd_stats_t* out) {
+    Red<X> R(x);
+    if (!driver_enter(x, R, c, out)) return;
+    const int64_t rebuilds0 = c.s.vl_meta[2];
+    const double margin = c.p.r_list;  // overlap_margin = r_list = sigma + skin (dynamics.py:366-367)
+    if (vl_stale(x, R, c) && !vl_rebuild(x, R, c, margin)) {
+        if (x.leader()) out->status = BD_ERR_CAPACITY;
+        return;
     }
-    u64* r = R.open();
-    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) x.add(r, (u64)c.s.overlap_flags[i]);
-    const u64 nov = R.close(r);
-    if (x.leader()) {
-        out->rebuilds = c.s.vl_meta[2] - rebuilds0;
-        out->dt_used = c.p.dt;
-        out->overlap_iterations = iters;
-        out->flip_passes = 0;
-        out->inversion_repairs = 0;
-        out->rollbacks = 0;
-        out->n_overlapping = (int64_t)nov;
-        out->status = (int64_t)c.w.ctl->status;
-        out->err_i = (int64_t)c.w.ctl->err_i;
-        out->err_k = (int64_t)c.w.ctl->err_k;
-        *c.s.call = c.call;
-    }
+    ph_abp_move(x, c);
+    c.call++;
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) c.s.overlap_flags[i] = 0;
+    const int64_t iters = overlap_rounds(x, R, c, margin);
+    verlet_stats(x, R, c, out, rebuilds0, iters);
 }
 
 }  // namespace bd

@@ -75,13 +75,14 @@ def _stream():
 
 
 def make_params(params: SimParams, box_length: float, seed: int, stream: int, force_mode: int = 0,
-                precision: int = 0, skin: float | None = None, pairs: bool = False) -> _abi.BdParams:
+                precision: int = 0, skin: float | None = None, pairs: bool = False,
+                no_cutoff: bool = False) -> _abi.BdParams:
     p = _abi.BdParams()
     p.n = params.n
     p.L = float(box_length)
     p.sigma, p.dt, p.diffusion = float(params.sigma), float(params.dt), float(params.diffusion)
     p.cap, p.clamp = float(params.displacement_cap), float(params.noise_clamp)
-    p.r_cut = float(params.r_cutoff) if params.r_cutoff is not None else 0.0
+    p.r_cut = float(params.r_cutoff) if params.r_cutoff is not None and not no_cutoff else 0.0
     p.skin = 0.5 * params.sigma if skin is None else float(skin)
     p.tol = 1e-12
     p.max_overlap_iters, p.max_rollbacks = int(params.max_overlap_iters), int(params.max_rollbacks)
@@ -407,3 +408,76 @@ class ShortRangeSimulation(_SimulationBase):
     def _launch_driver(self, stats_ptr: int):
         check(lib().bd_step_verlet(ctypes.byref(self._eng.s), ctypes.byref(self.bparams),
                                    ctypes.c_void_p(stats_ptr), _stream()), "bd_step_verlet")
+
+
+class AbpState:
+    """Director angles and self-propulsion parameters (dynamics.py:60-66).
+
+    Once a simulation owns it, the angles live on the device (`angles_t`);
+    the `angles` attribute reads / writes them as a numpy array, like the
+    reference's in-place numpy array."""
+
+    def __init__(self, angles, speed: float, rot_diffusion: float):
+        self.speed = float(speed)
+        self.rot_diffusion = float(rot_diffusion)
+        self._host = np.ascontiguousarray(angles, dtype=np.float64).reshape(-1).copy()
+        self.angles_t = None
+
+    def bind(self, device):
+        import torch
+        if self.angles_t is None:
+            self.angles_t = torch.from_numpy(self._host).to(device)
+        return self.angles_t
+
+    @property
+    def angles(self) -> np.ndarray:
+        return self.angles_t.cpu().numpy() if self.angles_t is not None else self._host
+
+    @angles.setter
+    def angles(self, value):
+        import torch
+        v = np.ascontiguousarray(value, dtype=np.float64).reshape(-1)
+        if self.angles_t is not None:
+            self.angles_t.copy_(torch.from_numpy(v))
+        else:
+            self._host = v.copy()
+
+
+class AbpSimulation(_SimulationBase):
+    """Active Brownian particles (dynamics.py:349-399), one persistent kernel
+    per step: Verlet list kept fresh, ballistic move by speed * dt along
+    (cos theta, sin theta), angles += sqrt(2 D_r dt) xi (unclamped unless
+    clamp_angle_noise), overlap rounds over the candidates within sigma + skin.
+
+    The angular noise xi is the counter generator's normals(n) of one call
+    per step (element i = pair i // 2, component i % 2)."""
+
+    def __init__(self, sys: ParticleSystem, params: SimParams, rng, abp: AbpState, skin: float | None = None,
+                 clamp_angle_noise: bool = False, debug_scan: bool = False, collect_flags: bool = False):
+        super().__init__(sys, params, rng, debug_scan, collect_flags)
+        self.abp = abp
+        if abp.angles.shape != (sys.n,):
+            raise BrownsimError(f"abp.angles must have shape ({sys.n},)")
+        self.skin = 0.5 * params.sigma if skin is None else float(skin)
+        self.r_list = params.sigma + self.skin
+        self.overlap_margin = self.r_list
+        self.clamp_angle_noise = bool(clamp_angle_noise)
+        self.tri = None
+        self.bparams = make_params(params, sys.box.length, self.rng.seed, self.rng.stream, _abi.BD_FORCE_SR,
+                                   _abi.BD_LR_EXACT, self.skin, pairs=True, no_cutoff=True)
+        self._refresh_params()
+        self._eng = _Engine(sys, None, self.bparams, self.rng.call)
+        self._eng.s.angles = abp.bind(sys.device).data_ptr()
+        self._eng.clear_status()
+
+    def _refresh_params(self):
+        super()._refresh_params()
+        self.bparams.abp_speed = float(self.abp.speed)
+        self.bparams.abp_rot_diffusion = float(self.abp.rot_diffusion)
+        self.bparams.abp_clamp_angle = int(self.clamp_angle_noise)
+
+    verlet = ShortRangeSimulation.verlet
+
+    def _launch_driver(self, stats_ptr: int):
+        check(lib().bd_step_abp(ctypes.byref(self._eng.s), ctypes.byref(self.bparams),
+                                ctypes.c_void_p(stats_ptr), _stream()), "bd_step_abp")

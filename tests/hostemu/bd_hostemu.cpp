@@ -60,6 +60,12 @@ void bdh_step_verlet(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out)
     step_verlet(x, c, out);
 }
 
+void bdh_step_abp(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out) {
+    Ctx c = host_ctx(s, p);
+    ExecHost x{c.w.ctl};
+    step_abp(x, c, out);
+}
+
 int64_t bdh_restore_delaunay(const bd_state_t* s, const bd_params_t* p) {
     Ctx c = host_ctx(s, p);
     c.call = 0;

@@ -21,8 +21,14 @@ LIB = os.path.join(HERE, "hostemu", "_build", "libbd_hostemu.so")
 TRI_KEYS = ("tri_v", "tri_shift", "tri_edge", "edge_v", "edge_tri", "edge_opp")
 
 
-@pytest.fixture(scope="module")
-def emu():
+_LIB = None
+
+
+def load_emu():
+    """Build (make) and load the host-emulation library with its prototypes."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
     subprocess.run(["make", "-s", "-C", os.path.join(HERE, "hostemu")], check=True, capture_output=True)
     lib = ctypes.CDLL(LIB)
     P = ctypes.POINTER
@@ -41,7 +47,14 @@ def emu():
     lib.bdh_normals.argtypes = [ctypes.c_uint64] * 4 + [c_i64, c_vp]
     lib.bdh_restore_delaunay.argtypes = [P(BdState), P(BdParams)]
     lib.bdh_restore_delaunay.restype = c_i64
+    lib.bdh_step_abp.argtypes = [P(BdState), P(BdParams), P(BdStats)]
+    _LIB = lib
     return lib
+
+
+@pytest.fixture(scope="module")
+def emu():
+    return load_emu()
 
 
 def params_for(lib, L, seed=0, dt=0.01, r_cut=2.5, n=0, force_mode=0, pairs=False):
