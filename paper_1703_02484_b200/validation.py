@@ -57,3 +57,18 @@ def audit_geometry(sim) -> tuple:
                                       ctypes.c_void_p(out.data_ptr()), _stream()), "bd_tri_audit_geometry")
     a, c = (int(v) for v in out.cpu().numpy())
     return a, c
+
+
+def cell_overlaps(positions_t, L: float, thresh: float) -> int:
+    """Number of pairs closer than `thresh`, via the device cell-list pair
+    build (bd_verlet_build at radius thresh) -- the O(N) form of the debug
+    scan for large N (brute force is O(N^2))."""
+    from .core import PeriodicBox
+    from .forces import build_verlet
+    vl = build_verlet(positions_t, PeriodicBox(float(L)), float(thresh), 0.0)
+    if vl.n_pairs == 0:
+        return 0
+    p = positions_t
+    d = p[vl.pair_b] - p[vl.pair_a]
+    d = d - (d / L + 0.5).floor() * L
+    return int(((d * d).sum(1) < thresh * thresh).sum().item())
