@@ -9,7 +9,9 @@ import os
 from . import _abi
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libbd_b200.so")
+# BD_LIB_PATH: an alternative build of the same library (kernel-variant
+# experiments in tools/); the default is the in-tree build
+LIB_PATH = os.environ.get("BD_LIB_PATH") or os.path.join(_HERE, "_lib", "libbd_b200.so")
 _lib = None
 
 

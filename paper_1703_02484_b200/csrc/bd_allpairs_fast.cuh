@@ -120,25 +120,50 @@ __global__ void k_sort_count(const double* __restrict__ pos, int64_t n, double L
     }
 }
 
-// single-CTA exclusive scan of the cell counts (<= 2^30 cells; one pass of
-// 1024-wide chunks with a running carry)
+// single-CTA exclusive scan of the cell counts: warp w owns a contiguous
+// segment of the cells and walks it in coalesced 32-cell chunks (8 loads in
+// flight); pass 1 sums the segments, one warp scans the 32 segment totals,
+// pass 2 writes the offsets (and zeroes the scatter cursors)
 __global__ void __launch_bounds__(1024) k_sort_scan(SortWs w, int64_t ncells) {
-    // each thread owns a contiguous run of cells: serial sums, one block
-    // scan of the 1024 run totals, serial write-back (3 barriers in total)
-    __shared__ int64_t sh[32];
-    const int64_t per = (ncells + blockDim.x - 1) / blockDim.x;
-    const int64_t c0 = threadIdx.x * per, c1 = c0 + per < ncells ? c0 + per : ncells;
-    int64_t run = 0;
-    for (int64_t c = c0; c < c1; ++c) run += w.cell_off[c];
-    int64_t ex;
-    const int64_t tot = block_excl_scan(run, ex, sh);
-    for (int64_t c = c0; c < c1; ++c) {
-        const int32_t v = w.cell_off[c];
-        w.cell_off[c] = (int32_t)ex;
-        w.cell_cur[c] = 0;
-        ex += v;
+    __shared__ int64_t seg[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t per = ((ncells + 31) / 32 + 31) & ~(int64_t)31;
+    const int64_t c0 = wid * per, c1 = c0 + per < ncells ? c0 + per : ncells;
+    int64_t sum = 0;
+#pragma unroll 8
+    for (int64_t c = c0 + lane; c < c1; c += 32) sum += w.cell_off[c];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) seg[wid] = sum;
+    __syncthreads();
+    if (wid == 0) {
+        const int64_t v = seg[lane];
+        int64_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        seg[lane] = inc - v;
+        if (lane == 31) w.cell_off[ncells] = (int32_t)inc;
     }
-    if (threadIdx.x == 0) w.cell_off[ncells] = (int32_t)tot;
+    __syncthreads();
+    int64_t carry = seg[wid];
+    for (int64_t base = c0; base < c1; base += 32) {
+        const int64_t c = base + lane;
+        const int64_t v = c < c1 ? w.cell_off[c] : 0;
+        int64_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (c < c1) {
+            w.cell_off[c] = (int32_t)(carry + inc - v);
+            w.cell_cur[c] = 0;
+        }
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
 }
 
 __global__ void k_sort_scatter(int64_t n, SortWs w) {

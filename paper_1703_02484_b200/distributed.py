@@ -34,8 +34,16 @@ class Shard:
         return s0, min(n, s0 + self.chunk)
 
 
+# receiver slots per rank are a multiple of this: every rank's receiver
+# blocks then coincide with the single-GPU blocks (FS_RPB = 128 slots per CTA
+# in csrc/bd_allpairs_fast.cuh), so per-block decisions (the generic
+# image path) and hence the bits are the same for every world size
+SLOT_ALIGN = 256
+
+
 def shard_for(n: int, rank: int, world: int) -> Shard:
-    return Shard(rank, world, (n + world - 1) // world)
+    chunk = (n + world - 1) // world
+    return Shard(rank, world, (chunk + SLOT_ALIGN - 1) // SLOT_ALIGN * SLOT_ALIGN)
 
 
 class ShardedLongRange:

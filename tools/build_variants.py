@@ -1,0 +1,28 @@
+"""Build kernel-variant copies of libbd_b200.so for timing experiments
+(tools/time_variants.sh -> tools/time_force.py with BD_LIB_PATH=...).
+Output: paper_1703_02484_b200/_lib/variants/ (not used by the product)."""
+import os
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1703_02484_b200 import build  # noqa: E402
+
+VARIANTS = {
+    "inline_sel": ["BD_FS_INLINE_SEL=1"],
+    "inline_sel_ts256_s2": ["BD_FS_INLINE_SEL=1", "BD_FS_TS=256", "BD_FS_S=2"],
+    "bt128_ts128_s4": ["BD_FS_BT=128", "BD_FS_TS=128", "BD_FS_S=4"],
+    "bt128_ts256_s2": ["BD_FS_BT=128", "BD_FS_TS=256", "BD_FS_S=2"],
+    "bt256_ts256_s4": ["BD_FS_BT=256", "BD_FS_TS=256", "BD_FS_S=4"],
+    "bt256_ts256_s3": ["BD_FS_BT=256", "BD_FS_TS=256", "BD_FS_S=3"],
+    "bt256_ts128_s4": ["BD_FS_BT=256", "BD_FS_TS=128", "BD_FS_S=4"],
+    "bt512_ts256_s4": ["BD_FS_BT=512", "BD_FS_TS=256", "BD_FS_S=4"],
+}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(VARIANTS)
+    out = os.path.join(os.path.dirname(build.LIB), "variants")
+    with ThreadPoolExecutor(6) as ex:
+        for name, path in zip(names, ex.map(lambda k: build.build(out=os.path.join(out, f"libbd_{k}.so"),
+                                                                    defines=VARIANTS[k]), names)):
+            print(name, path)

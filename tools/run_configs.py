@@ -109,7 +109,7 @@ def run(cfg_id, args):
     stats_tot = dict(overlap_iterations=0, flip_passes=0, inversion_repairs=0, rollbacks=0)
     done = 0
     while done < K:
-        chunk = min(every, K - done)
+        chunk = min(every - done % every, K - done)
         for nxt in msd_t:
             if nxt > done:
                 chunk = min(chunk, nxt - done)
