@@ -5,9 +5,12 @@ tests/golden/make_golden_msd.py from the reference with the counter noise).
   oracle  -> final positions bit-exact after 1,000 steps
   gpu EXACT -> final positions bit-exact after 1,000 steps; MSD(t) from the
           device image counters equal to the reference's MSD to 1e-9
-  gpu FAST  -> MSD(t) within 3 % of the reference's at every checkpoint
-          (FAST sums the all-pairs force in another order, |dF|/|F| ~ 1e-13;
-          the trajectories then drift apart, the statistics must not)
+  gpu FAST  -> MSD(t) within 3 standard deviations of the reference's
+          run-to-run spread at every checkpoint (FAST sums the all-pairs force
+          in another order, |dF|/|F| ~ 1e-13; the trajectories then drift
+          apart, the statistics must not).  The spread is measured on the
+          reference itself: the same initial state with 4 more noise seeds
+          (msd_other_seeds; 10 % at t = 1000, 0.5 % at t <= 50)
 """
 
 import os
@@ -19,7 +22,6 @@ from golden_io import TRI_KEYS
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 G = dict(np.load(os.path.join(HERE, "golden", "msd_lr_n1024.npz")))
-FAST_MSD_RTOL = 0.03
 
 
 def test_oracle_1000_steps_bitwise():
@@ -63,6 +65,7 @@ def test_gpu_exact_1000_steps_bitwise_and_msd():
 @pytest.mark.gpu
 def test_gpu_fast_msd_statistics():
     sim, msd = run_gpu("fast")
-    rel = np.abs(msd - G["msd"]) / G["msd"]
-    assert (rel <= FAST_MSD_RTOL).all(), rel
+    runs = np.vstack([G["msd"][None], G["msd_other_seeds"]])
+    sd = runs.std(axis=0, ddof=1)
+    assert (np.abs(msd - G["msd"]) <= 3.0 * sd).all(), (msd, G["msd"], sd)
     assert sim.tri.audit(sim.sys.positions).ok
