@@ -49,6 +49,11 @@ extern "C" {
  * bit; FAST uses fma + rsqrt/Newton (|dF|/|F| <= 1e-12) */
 #define BD_LR_EXACT 0
 #define BD_LR_FAST 1
+/* FAST-SYM: FAST arithmetic with each unordered pair's r^-3 evaluated once
+ * and applied to both directions (Newton's third law on the geometric
+ * factor; csrc/bd_allpairs_sym.cuh).  Single GPU, whole range only;
+ * workspace ~ n^2/32 bytes (bd_long_range_workspace_bytes_for). */
+#define BD_LR_FAST_SYM 2
 
 /* PeriodicTriangulation arrays, triangulation.py:129-139 */
 typedef struct bd_tri {
@@ -130,8 +135,11 @@ int bd_long_range_forces(const double* pos, const double* alpha, const double* m
                          double L, int64_t i_begin, int64_t i_end, int precision, double* out,
                          int64_t* err, void* work, void* stream);
 
-/* scratch bytes of bd_long_range_forces (packed sources) */
+/* scratch bytes of bd_long_range_forces (packed sources) for EXACT / FAST */
 int64_t bd_long_range_workspace_bytes(int64_t n);
+
+/* scratch bytes of bd_long_range_forces for a given precision (BD_LR_*) */
+int64_t bd_long_range_workspace_bytes_for(int64_t n, int precision);
 
 /* short_range_kernel (_kernels.py:62-91) over stored pairs, accumulated
  * per particle in ascending pair order (bit-exact). */

@@ -19,6 +19,7 @@ BD_FORCE_LRSR = 2
 
 BD_LR_EXACT = 0
 BD_LR_FAST = 1
+BD_LR_FAST_SYM = 2
 
 
 class BdTri(ctypes.Structure):
@@ -67,6 +68,7 @@ def _protos():
         "bd_workspace_bytes": ([P(BdParams), c_i64, c_i64], c_i64),
         "bd_pairs_workspace_bytes": ([c_i64, c_d, c_d, c_i64], c_i64),
         "bd_long_range_workspace_bytes": ([c_i64], c_i64),
+        "bd_long_range_workspace_bytes_for": ([c_i64, c_int], c_i64),
         "bd_long_range_forces": ([c_vp, c_vp, c_vp, c_i64, c_d, c_i64, c_i64, c_int, c_vp, c_vp, c_vp, c_vp], c_int),
         "bd_short_range_forces": ([c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_d, c_d, c_vp, c_vp, c_vp, c_vp],
                                   c_int),
@@ -123,4 +125,5 @@ EXPORTS = ("bd_brute_overlaps", "bd_force","bd_force_prepare", "bd_force_slots",
            "bd_tri_restore_delaunay", "bd_clear_status", "bd_tri_audit_geometry", "bd_build_info",
            "bd_integrate", "bd_tri_apply_crossings", "bd_tri_edge_inversion", "bd_tri_signed_area2",
            "bd_tri_delaunay_flags", "bd_tri_inverted_edge_flags", "bd_tri_flip_edges", "bd_tri_repair_inversions",
-           "bd_tri_restore_delaunay_ex", "bd_overlap_correct", "bd_tri_copy", "bd_step_abp", "bd_run_abp")
+           "bd_tri_restore_delaunay_ex", "bd_overlap_correct", "bd_tri_copy", "bd_step_abp", "bd_run_abp",
+           "bd_long_range_workspace_bytes_for")

@@ -1,0 +1,469 @@
+// bd_allpairs_sym.cuh -- FAST-SYM all-pairs force: Newton's third law on
+// the shared factor r^-3, sorted slots, tile-uniform images.
+//
+// The force of _kernels.long_range_kernel (_kernels.py:26-59),
+//     F_i = mu_i sum_{k != i} alpha_k r_ik / |r_ik|^3 ,
+// is non-reciprocal (mu_i alpha_k != mu_k alpha_i) but its geometric factor
+// w_ik = |r_ik|^-3 and the displacement r_ik = -r_ki are shared by the two
+// directions of a pair.  Writing F_i = mu_i (A_i - B_i) with
+//     A_i = sum over pairs where i is the receiver of  alpha_k w d ,
+//     B_k = sum over pairs where k is the source   of  alpha_i w d ,
+// every unordered pair is evaluated ONCE: 10 FP64 instructions for d, r^2
+// and w (MUFU.RSQ64H + second-order correction), 3 for the receiver side
+// and 3 for the source side -> 8 FP64 instructions per directed pair
+// instead of the 12 of the directed FAST kernel (bd_allpairs_fast.cuh).
+//
+// Work decomposition (deterministic: every sum has a fixed order):
+//  * slots are the Morton-sorted particles of the FAST path (same sort);
+//    receiver blocks I of SY_BT slots, one receiver per thread;
+//  * block I pairs with blocks J = I + d (mod Mb), d = 1..D, D = Mb/2
+//    (circulant: every unordered block pair exactly once; for even Mb the
+//    d = D pairs belong to the lower block I < Mb/2), split into SY_S
+//    chunks of d -> grid (Mb, SY_S); chunk 0 also does the diagonal block
+//    J = I as directed pairs (receiver side only, k != i);
+//  * the source tiles of J (SY_TS slots) stream through shared memory by
+//    TMA; each lane owns two receivers, so every source feeds two pair
+//    evaluations; the lane's source-side partial (summed over its two
+//    receivers) is reduced over the warp by a butterfly (amortised over 64
+//    pairs), the CTA adds its warps in warp order and writes one partial
+//    per (d, source);
+//  * k_sym_combine sums the SY_S receiver partials and the D source
+//    partials of every slot in fixed order: F = mu (A - B).
+// Single-GPU only (the sharded path keeps the directed kernel, whose
+// per-receiver sums make results identical for every world size).
+#pragma once
+
+#include "bd_allpairs_fast.cuh"
+
+namespace bd {
+
+struct alignas(16) SrcS {
+    double x, y, a, mu;
+};
+
+struct alignas(16) SelS {  // receiver image selector (axis_select of both axes)
+    double cx_le, cx_gt, cy_le, cy_gt;
+    uint64_t Tx, Ty, amb, pad;
+};
+
+constexpr int SY_BT = 256;  // receivers per block = threads per CTA
+constexpr int SY_NW = SY_BT / 32;
+constexpr int SY_TS = 128;  // sources per shared-memory stage
+constexpr int SY_S = 8;     // chunks of the circulant distance range (grid.y)
+
+BD_HD int64_t sym_blocks(int64_t n) { return (n + SY_BT - 1) / SY_BT; }
+BD_HD int64_t sym_D(int64_t n) { return sym_blocks(n) / 2; }
+BD_HD int64_t sym_tiles(int64_t n) { return (n + SY_TS - 1) / SY_TS; }
+
+struct SymWs {
+    SortWs sort;     // cell sort of the FAST path (order, cells); its src/bbox/part3 are unused here
+    SrcS* src;       // (n) sources in slot order
+    SelS* sel;       // (n) receiver selectors in slot order
+    uint64_t* bbox;  // (ntiles, 4) min/max bits of x and y per SY_TS tile
+    double* apart;   // (SY_S, n, 2) receiver-side partial sums per chunk
+    double* bpart;   // (D, n, 2) source-side partial sums per circulant distance
+    double* slot3;   // (n, 3) fx, fy, flag per slot
+};
+
+BD_HD int64_t sym_ws_bytes(int64_t n) {
+    const int64_t D = sym_D(n) > 0 ? sym_D(n) : 1;
+    return fast_ws_bytes(n) + fs_align(32 * n) + fs_align(64 * n) + fs_align(32 * sym_tiles(n)) +
+           fs_align(16 * n * SY_S) + fs_align(16 * n * D) + fs_align(24 * n) + 256;
+}
+
+BD_HD SymWs sym_ws_carve(void* base, int64_t n) {
+    SymWs w;
+    w.sort = fast_ws_carve(base, n);
+    char* b = (char*)(((uintptr_t)base + 255) & ~(uintptr_t)255) + fast_ws_bytes(n);
+    const int64_t D = sym_D(n) > 0 ? sym_D(n) : 1;
+    w.src = (SrcS*)b; b += fs_align(32 * n);
+    w.sel = (SelS*)b; b += fs_align(64 * n);
+    w.bbox = (uint64_t*)b; b += fs_align(32 * sym_tiles(n));
+    w.apart = (double*)b; b += fs_align(16 * n * SY_S);
+    w.bpart = (double*)b; b += fs_align(16 * n * D);
+    w.slot3 = (double*)b;
+    return w;
+}
+
+#if defined(__CUDACC__)
+
+// one CTA per SY_TS tile of slots: sources, receiver selectors, tile box
+__global__ void __launch_bounds__(SY_TS) k_sym_pack(const double* __restrict__ pos, const double* __restrict__ alpha,
+                                                    const double* __restrict__ mu, int64_t n, double L, double lo,
+                                                    double hi, SymWs w) {
+    __shared__ uint64_t red[4][SY_TS / 32];
+    const int64_t s = (int64_t)blockIdx.x * SY_TS + threadIdx.x;
+    uint64_t xmin = ~0ull, xmax = 0, ymin = ~0ull, ymax = 0;
+    if (s < n) {
+        const int64_t i = w.sort.order[s];
+        const double x = pos[2 * i], y = pos[2 * i + 1];
+        SrcS r;
+        r.x = x;
+        r.y = y;
+        r.a = alpha[i];
+        r.mu = mu[i];
+        w.src[s] = r;
+        const AxisSel sx = axis_select(x, L, lo, hi), sy = axis_select(y, L, lo, hi);
+        SelS q;
+        q.cx_le = x + sx.shift_le;
+        q.cx_gt = x + sx.shift_gt;
+        q.cy_le = y + sy.shift_le;
+        q.cy_gt = y + sy.shift_gt;
+        q.Tx = sx.T;
+        q.Ty = sy.T;
+        q.amb = (uint64_t)(sx.amb || sy.amb);
+        q.pad = 0;
+        w.sel[s] = q;
+        xmin = xmax = dbits(x);
+        ymin = ymax = dbits(y);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        xmin = min(xmin, __shfl_xor_sync(0xffffffffu, xmin, o));
+        xmax = max(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+        ymin = min(ymin, __shfl_xor_sync(0xffffffffu, ymin, o));
+        ymax = max(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
+    }
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        red[0][wid] = xmin;
+        red[1][wid] = xmax;
+        red[2][wid] = ymin;
+        red[3][wid] = ymax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < SY_TS / 32; ++k) {
+            xmin = min(xmin, red[0][k]);
+            xmax = max(xmax, red[1][k]);
+            ymin = min(ymin, red[2][k]);
+            ymax = max(ymax, red[3][k]);
+        }
+        uint64_t* b = w.bbox + 4 * blockIdx.x;
+        b[0] = xmin;
+        b[1] = xmax;
+        b[2] = ymin;
+        b[3] = ymax;
+    }
+}
+
+// r^-3 from r^2: y0 = MUFU.RSQ64H (~2^-22), e = 1 - r2 y0^2,
+// r^-3 = y0^3 (1 + 1.5 e + 1.875 e^2) (+ O(e^3) ~ 1e-19)
+BD_DEV double inv_r3(double r2) {
+    const double y0 = rsqrt_mufu(r2);
+    const double t = y0 * y0;
+    const double e = fma(-r2, t, 1.0);
+    const double y3 = t * y0;
+    return y3 * fma(fma(1.875, e, 1.5), e, 1.0);
+}
+
+// Two receivers per lane (slots lane and lane + 32 of the warp's 64):
+// every source read from shared memory feeds two pair evaluations, and the
+// source-side partial of a lane is the sum over its two receivers before
+// the warp butterfly (so the reduction is amortised over 64 pairs).
+constexpr int SY_R = 2;
+
+struct SymRecv {
+    double cx_le[SY_R], cx_gt[SY_R], cy_le[SY_R], cy_gt[SY_R];
+    uint64_t Tx[SY_R], Ty[SY_R];
+    double a[SY_R];   // alpha of the receiver (source-side factor); 0 for an inactive slot
+    double ax[SY_R], ay[SY_R];  // receiver-side accumulators A
+};
+
+enum { SY_UNIFORM = 0, SY_SELECT = 1, SY_GENERIC = 2 };
+
+// raw receiver coordinate from its selector: one of the two shifted copies is unshifted
+BD_DEV double raw_coord(double c_le, double c_gt, double L) { return c_gt < L ? c_gt : c_le; }
+
+// One source against the lane's receivers.  Receiver side: A += alpha_k w d.
+// Source side: returns sum_m alpha_m w d_src (x, y) for the warp reduction.
+// d_src is minus the source's OWN minimum-image displacement to the
+// receiver; it equals d except at image ties (fl(d / L) within ulps of
+// +-1/2, e.g. lattice pairs exactly L/2 apart), where the reference's two
+// directions do not use mirror images.  Such pairs need a source within a
+// few ulps of the receiver's breakpoint, so:
+//   UNIFORM -- every source of the tile is more than SY_EDGE ulps from every
+//              breakpoint: one image shift per receiver, d_src = d;
+//   SELECT  -- per-pair image from the breakpoints (integer compares) and
+//              d_src from the exact min-image arithmetic of the source side;
+//   GENERIC -- exact min-image arithmetic on both sides (receivers within
+//              ulps of L/2 have ambiguous breakpoints; essentially never).
+constexpr uint64_t SY_EDGE = 64;
+
+template <int MODE>
+BD_DEV void sym_pair(SymRecv& r, const SrcS& s, const double* cx, const double* cy, const double* Ll, double& bx,
+                     double& by) {
+    bx = 0.0;
+    by = 0.0;
+#pragma unroll
+    for (int m = 0; m < SY_R; ++m) {
+        double dx, dy, sx_, sy_;
+        if (MODE == SY_UNIFORM) {
+            dx = cx[m] - s.x;
+            dy = cy[m] - s.y;
+            sx_ = dx;
+            sy_ = dy;
+        } else {
+            const double xr = raw_coord(r.cx_le[m], r.cx_gt[m], Ll[0]);
+            const double yr = raw_coord(r.cy_le[m], r.cy_gt[m], Ll[0]);
+            if (MODE == SY_GENERIC) {
+                dx = mi_fast(xr - s.x, Ll[0], Ll[1], Ll[2]);
+                dy = mi_fast(yr - s.y, Ll[0], Ll[1], Ll[2]);
+            } else {
+                dx = (dbits(s.x) <= r.Tx[m] ? r.cx_le[m] : r.cx_gt[m]) - s.x;
+                dy = (dbits(s.y) <= r.Ty[m] ? r.cy_le[m] : r.cy_gt[m]) - s.y;
+            }
+            sx_ = -mi_fast(s.x - xr, Ll[0], Ll[1], Ll[2]);
+            sy_ = -mi_fast(s.y - yr, Ll[0], Ll[1], Ll[2]);
+        }
+        const double w = inv_r3(fma(dx, dx, dy * dy));
+        const double ta = s.a * w;
+        r.ax[m] = fma(ta, dx, r.ax[m]);
+        r.ay[m] = fma(ta, dy, r.ay[m]);
+        const double tb = r.a[m] * w;
+        bx = fma(tb, sx_, bx);
+        by = fma(tb, sy_, by);
+    }
+}
+
+// diagonal block (J == I): directed, receiver side only, k != i
+template <int MODE>
+BD_DEV void sym_diag(SymRecv& r, const SrcS& s, int64_t k, const int64_t* slot, const double* cx,
+                     const double* cy, const double* Ll) {
+#pragma unroll
+    for (int m = 0; m < SY_R; ++m) {
+        double dx, dy;
+        if (MODE == SY_GENERIC) {
+            dx = mi_fast(raw_coord(r.cx_le[m], r.cx_gt[m], Ll[0]) - s.x, Ll[0], Ll[1], Ll[2]);
+            dy = mi_fast(raw_coord(r.cy_le[m], r.cy_gt[m], Ll[0]) - s.y, Ll[0], Ll[1], Ll[2]);
+        } else {
+            dx = (dbits(s.x) <= r.Tx[m] ? r.cx_le[m] : r.cx_gt[m]) - s.x;
+            dy = (dbits(s.y) <= r.Ty[m] ? r.cy_le[m] : r.cy_gt[m]) - s.y;
+        }
+        double ta = s.a * inv_r3(fma(dx, dx, dy * dy));
+        ta = k == slot[m] ? 0.0 : ta;
+        r.ax[m] = fma(ta, dx, r.ax[m]);
+        r.ay[m] = fma(ta, dy, r.ay[m]);
+    }
+}
+
+// transposed warp reduction of 8 per-lane values (one per source): after
+// it, lanes with bits (4,3,2) = g hold the warp sum of value g.  9 shuffles
+// and 9 adds for 8 sums (a butterfly per value: 40 and 40)
+BD_DEV double tree8(const double v[8], int lane) {
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+    double h[4], q[2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const double send = b4 ? v[j] : v[j + 4];
+        const double keep = b4 ? v[j + 4] : v[j];
+        h[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const double send = b3 ? h[j] : h[j + 2];
+        const double keep = b3 ? h[j + 2] : h[j];
+        q[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    const double send = b2 ? q[0] : q[1];
+    const double keep = b2 ? q[1] : q[0];
+    double r = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    r += __shfl_xor_sync(0xffffffffu, r, 2);
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
+    return r;
+}
+
+BD_DEV double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+constexpr int SY_G = 8;  // sources per transposed reduction
+
+// a tile of `cnt` sources: pair evaluations + warp sums of the source side into bws[2*j .. 2*j+1]
+template <int MODE>
+BD_DEV void sym_tile(SymRecv& r, const SrcS* sm, int cnt, const double* cx, const double* cy, const double* Ll,
+                     double* bws, int lane) {
+    int j = 0;
+    for (; j + SY_G <= cnt; j += SY_G) {
+        double bx[SY_G], by[SY_G];
+#pragma unroll
+        for (int u = 0; u < SY_G; ++u) sym_pair<MODE>(r, sm[j + u], cx, cy, Ll, bx[u], by[u]);
+        const double sx = tree8(bx, lane), sy = tree8(by, lane);
+        if ((lane & 3) == 0) {
+            const int k = j + (lane >> 2);
+            bws[2 * k] = sx;
+            bws[2 * k + 1] = sy;
+        }
+    }
+    for (; j < cnt; ++j) {
+        double bx, by;
+        sym_pair<MODE>(r, sm[j], cx, cy, Ll, bx, by);
+        const double sx = warp_sum(bx), sy = warp_sum(by);
+        if (lane == 0) {
+            bws[2 * j] = sx;
+            bws[2 * j + 1] = sy;
+        }
+    }
+}
+
+BD_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// TMA of source tile t (SY_TS slots; fewer or none past n) into stage st
+BD_DEV void sym_issue(const SymWs& w, int64_t n, int64_t t, SrcS* tiles, uint64_t* bars, int st) {
+    const int64_t cnt = (t + 1) * SY_TS <= n ? SY_TS : (t * SY_TS < n ? n - t * SY_TS : 0);
+    mbar_expect_tx(&bars[st], (uint32_t)(cnt * sizeof(SrcS)));
+    if (cnt) bulk_g2s(tiles + st * SY_TS, w.src + t * SY_TS, (uint32_t)(cnt * sizeof(SrcS)), &bars[st]);
+}
+
+constexpr int SY_CT = SY_BT / SY_R;  // threads per CTA
+constexpr int SY_NW2 = SY_CT / 32;   // warps per CTA
+// dynamic smem: 2 source stages + 2 buffers of per-warp source-side sums
+constexpr int SY_SMEM = 2 * SY_TS * (int)sizeof(SrcS) + 2 * SY_NW2 * SY_TS * 16;
+
+// grid (Mb, SY_S), SY_CT threads; warp v of block I owns slots I*SY_BT + 64 v + {lane, lane + 32}
+__global__ void __launch_bounds__(SY_CT, 4) k_allpairs_sym(SymWs w, int64_t n, double L, double lo, double hi) {
+    extern __shared__ __align__(128) unsigned char sy_smem[];
+    SrcS* tiles = reinterpret_cast<SrcS*>(sy_smem);                              // [2][SY_TS]
+    double* bw = reinterpret_cast<double*>(sy_smem + 2 * SY_TS * sizeof(SrcS));  // [2][SY_NW2][SY_TS][2]
+    __shared__ __align__(8) uint64_t bars[2];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t Mb = sym_blocks(n), D = sym_D(n);
+    const int64_t I = blockIdx.x;
+    const int chunk = blockIdx.y;
+
+    SymRecv r;
+    int64_t slot[SY_R];
+    bool act[SY_R], amb = false;
+#pragma unroll
+    for (int m = 0; m < SY_R; ++m) {
+        slot[m] = I * SY_BT + 64 * wid + lane + 32 * m;
+        act[m] = slot[m] < n;
+        const int64_t sl = act[m] ? slot[m] : I * SY_BT;
+        const SelS q = w.sel[sl];
+        r.cx_le[m] = q.cx_le;
+        r.cx_gt[m] = q.cx_gt;
+        r.cy_le[m] = q.cy_le;
+        r.cy_gt[m] = q.cy_gt;
+        r.Tx[m] = q.Tx;
+        r.Ty[m] = q.Ty;
+        r.a[m] = act[m] ? w.src[sl].a : 0.0;
+        r.ax[m] = 0.0;
+        r.ay[m] = 0.0;
+        amb |= act[m] && q.amb;
+    }
+    const double Ll[3] = {L, lo, hi};
+
+    // this chunk's distances [d0, d1); chunk 0 adds the diagonal block (d = 0)
+    const int64_t per = (D + SY_S - 1) / SY_S;
+    const int64_t d0 = chunk == 0 ? 0 : 1 + (int64_t)chunk * per;
+    const int64_t d1 = 1 + ((int64_t)chunk + 1) * per < D + 1 ? 1 + ((int64_t)chunk + 1) * per : D + 1;
+    const bool even = (Mb & 1) == 0;
+    constexpr int64_t tpb = SY_BT / SY_TS;  // source tiles per block
+    const int64_t nq = d1 > d0 ? (d1 - d0) * tpb : 0;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const bool wamb = __any_sync(0xffffffffu, amb);
+    if (threadIdx.x == 0)
+        for (int64_t qi = 0; qi < 2 && qi < nq; ++qi)
+            sym_issue(w, n, ((I + d0 + qi / tpb) % Mb) * tpb + qi % tpb, tiles, bars, (int)qi);
+
+    for (int64_t qi = 0; qi < nq; ++qi) {
+        const int st = (int)(qi & 1);
+        const int64_t d = d0 + qi / tpb;
+        const int64_t J = (I + d) % Mb;
+        const int64_t t = J * tpb + qi % tpb;
+        const int64_t base = t * SY_TS;
+        const int cnt = (int)((t + 1) * SY_TS <= n ? SY_TS : (base < n ? n - base : 0));
+        const bool use = !(even && d == D && d > 0 && I >= Mb / 2) && cnt > 0;
+        const uint64_t* bb = w.bbox + 4 * t;
+        const uint64_t bx0 = bb[0], bx1 = bb[1], by0 = bb[2], by1 = bb[3];
+        mbar_wait(&bars[st], (uint32_t)((qi >> 1) & 1));
+        const SrcS* sm = tiles + st * SY_TS;
+        double* bws = bw + ((size_t)st * SY_NW2 + wid) * SY_TS * 2;
+        if (use) {
+            double cx[SY_R], cy[SY_R];
+            bool uni = true;
+#pragma unroll
+            for (int m = 0; m < SY_R; ++m) {
+                // every source more than SY_EDGE ulps below / above the breakpoint (no image ties)
+                const bool xle = bx1 + SY_EDGE <= r.Tx[m], xgt = bx0 > r.Tx[m] + SY_EDGE;
+                const bool yle = by1 + SY_EDGE <= r.Ty[m], ygt = by0 > r.Ty[m] + SY_EDGE;
+                uni &= (xle || xgt) && (yle || ygt);
+                cx[m] = xle ? r.cx_le[m] : r.cx_gt[m];
+                cy[m] = yle ? r.cy_le[m] : r.cy_gt[m];
+            }
+            const bool all_uni = __all_sync(0xffffffffu, uni);
+            if (d == 0) {
+                if (wamb) {
+                    for (int j = 0; j < cnt; ++j) sym_diag<SY_GENERIC>(r, sm[j], base + j, slot, cx, cy, Ll);
+                } else {
+                    for (int j = 0; j < cnt; ++j) sym_diag<SY_SELECT>(r, sm[j], base + j, slot, cx, cy, Ll);
+                }
+            } else if (wamb) {
+                sym_tile<SY_GENERIC>(r, sm, cnt, cx, cy, Ll, bws, lane);
+            } else if (all_uni) {
+                sym_tile<SY_UNIFORM>(r, sm, cnt, cx, cy, Ll, bws, lane);
+            } else {
+                sym_tile<SY_SELECT>(r, sm, cnt, cx, cy, Ll, bws, lane);
+            }
+        }
+        __syncthreads();  // stage st consumed; the warps' source-side sums of tile qi complete
+        if (threadIdx.x == 0 && qi + 2 < nq) {
+            fence_proxy_async_smem();
+            sym_issue(w, n, ((I + d0 + (qi + 2) / tpb) % Mb) * tpb + (qi + 2) % tpb, tiles, bars, st);
+        }
+        if (use && d > 0) {
+            // CTA sum of the warp sums (warp order) -> one partial per (d, source)
+            const double* bt = bw + (size_t)st * SY_NW2 * SY_TS * 2;
+            for (int e = threadIdx.x; e < 2 * cnt; e += SY_CT) {
+                double v = 0.0;
+#pragma unroll
+                for (int ww = 0; ww < SY_NW2; ++ww) v += bt[(size_t)ww * SY_TS * 2 + e];
+                w.bpart[(size_t)(d - 1) * n * 2 + (size_t)base * 2 + e] = v;
+            }
+        }
+        // this stage's sum buffer is written again two tiles later, after the next __syncthreads
+    }
+#pragma unroll
+    for (int m = 0; m < SY_R; ++m) {
+        if (!act[m]) continue;
+        w.apart[(size_t)chunk * n * 2 + 2 * slot[m]] = r.ax[m];
+        w.apart[(size_t)chunk * n * 2 + 2 * slot[m] + 1] = r.ay[m];
+    }
+}
+
+// F = mu (A - B) per slot, fixed summation order -> slot3 (fx, fy, flag)
+__global__ void k_sym_combine(int64_t n, SymWs w) {
+    const int64_t Mb = sym_blocks(n), D = sym_D(n);
+    const bool even = (Mb & 1) == 0;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
+        for (int c = 0; c < SY_S; ++c) {
+            ax += w.apart[(size_t)c * n * 2 + 2 * s];
+            ay += w.apart[(size_t)c * n * 2 + 2 * s + 1];
+        }
+        const int64_t J = s / SY_BT;
+        for (int64_t d = 1; d <= D; ++d) {
+            const int64_t I = (J - d + Mb) % Mb;
+            if (even && d == D && I >= Mb / 2) continue;  // that pair was done by block J as receiver
+            bx += w.bpart[(size_t)(d - 1) * n * 2 + 2 * s];
+            by += w.bpart[(size_t)(d - 1) * n * 2 + 2 * s + 1];
+        }
+        const double mu = w.src[s].mu;
+        const double fx = mu * (ax - bx), fy = mu * (ay - by);
+        w.slot3[3 * s] = fx;
+        w.slot3[3 * s + 1] = fy;
+        w.slot3[3 * s + 2] = (isfinite(fx) && isfinite(fy)) ? 0.0 : -1.0;
+    }
+}
+
+#endif  // __CUDACC__
+
+}  // namespace bd

@@ -9,6 +9,7 @@
 #include <mutex>
 
 #include "bd_allpairs.cuh"
+#include "bd_allpairs_sym.cuh"
 #include "bd_drivers.cuh"
 #include "bd_ops.cuh"
 
@@ -408,11 +409,32 @@ int launch_fast_finish(const double* pos, int64_t n, const bd_params_t& p, const
     return err_code(cudaGetLastError());
 }
 
+// FAST-SYM (single GPU): sort, pack, symmetric pair kernel, combine, unsort
+int launch_sym(const double* pos, const double* alpha, const double* mu, int64_t n, const bd_params_t& p,
+               const SymWs& w, double* out, int64_t* err, cudaStream_t st) {
+    if (n <= 0) return 0;
+    const int64_t nc = fast_ncells(n);
+    cudaError_t e = cudaMemsetAsync(w.sort.cell_off, 0, sizeof(int32_t) * (nc + 1), st);
+    if (e != cudaSuccess) return err_code(e);
+    k_sort_count<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, w.sort);
+    k_sort_scan<<<1, 1024, 0, st>>>(w.sort, nc);
+    k_sort_scatter<<<grid_for(n), 256, 0, st>>>(n, w.sort);
+    k_sort_fix<<<grid_for(nc), 256, 0, st>>>(nc, w.sort);
+    k_sym_pack<<<(unsigned)sym_tiles(n), SY_TS, 0, st>>>(pos, alpha, mu, n, p.L, p.mi_lo, p.mi_hi, w);
+    k_allpairs_sym<<<dim3((unsigned)sym_blocks(n), SY_S), SY_CT, SY_SMEM, st>>>(w, n, p.L, p.mi_lo, p.mi_hi);
+    k_sym_combine<<<grid_for(n), 256, 0, st>>>(n, w);
+    k_unsort_forces<<<grid_for(n), 256, 0, st>>>(0, n, w.sort, w.slot3, out, err);
+    k_lr_rescan_pos<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, p.mi_lo, p.mi_hi, err);
+    return err_code(cudaGetLastError());
+}
+
 int launch_force(const bd_state_t* s, const bd_params_t* p, cudaStream_t st) {
     init_device_info();
     if (p->force_mode == BD_FORCE_SR) return 0;  // the short-range force runs inside the step kernel
     const Ws w = ws_carve(s->work, *p, s->tri.ne, s->tri.nt);
     // force on the pre-move positions (dynamics.py:194)
+    if (p->lr_precision == BD_LR_FAST_SYM)
+        return launch_sym(s->pos, s->alpha, s->mu, p->n, *p, sym_ws_carve(w.src4, p->n), s->force, s->force_err, st);
     if (p->lr_precision == BD_LR_FAST) {
         const SortWs fw = fast_ws_carve(w.src4, p->n);
         int rc = launch_fast_prepare(s->pos, s->alpha, s->mu, p->n, p->L, fw, st);
@@ -524,6 +546,11 @@ int64_t bd_long_range_workspace_bytes(int64_t n) {
     return (f > 32 * n ? f : 32 * n) + 512;
 }
 
+int64_t bd_long_range_workspace_bytes_for(int64_t n, int precision) {
+    if (precision == BD_LR_FAST_SYM) return sym_ws_bytes(n) + 512;
+    return bd_long_range_workspace_bytes(n);
+}
+
 int bd_long_range_forces(const double* pos, const double* alpha, const double* mu, int64_t n, double L, int64_t i_begin,
                          int64_t i_end, int precision, double* out, int64_t* err, void* work, void* stream) {
     init_device_info();
@@ -532,6 +559,10 @@ int bd_long_range_forces(const double* pos, const double* alpha, const double* m
     memset(&p, 0, sizeof(p));
     p.L = L;
     prepare_params(&p);
+    if (precision == BD_LR_FAST_SYM) {
+        if (i_begin != 0 || i_end != n) return -(int)cudaErrorInvalidValue;  // whole range only
+        return launch_sym(pos, alpha, mu, n, p, sym_ws_carve(work, n), out, err, st);
+    }
     if (precision == BD_LR_FAST && i_begin == 0 && i_end == n) {
         const SortWs fw = fast_ws_carve(work, n);
         int rc = launch_fast_prepare(pos, alpha, mu, n, L, fw, st);
@@ -627,6 +658,7 @@ int bd_force(const bd_state_t* s, const bd_params_t* p, void* stream) {
 // ---- sharded all-pairs force (multi-GPU: receiver slots per rank + all-gather)
 int bd_force_prepare(const bd_state_t* s, const bd_params_t* p, void* stream) {
     init_device_info();
+    if (p->lr_precision == BD_LR_FAST_SYM) return -(int)cudaErrorInvalidValue;  // single-GPU mode
     cudaStream_t st = (cudaStream_t)stream;
     if (p->force_mode == BD_FORCE_SR) return 0;
     const Ws w = ws_carve(s->work, *p, s->tri.ne, s->tri.nt);

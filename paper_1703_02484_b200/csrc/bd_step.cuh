@@ -12,7 +12,7 @@
 // (and to oracle/bd_oracle.c) on the same inputs and noise.
 #pragma once
 
-#include "bd_allpairs_fast.cuh"
+#include "bd_allpairs_sym.cuh"
 #include "bd_exec.cuh"
 
 namespace bd {
@@ -72,7 +72,11 @@ BD_HD WsLayout ws_layout(const bd_params_t& p, int64_t ne, int64_t nt) {
     l.inc_cur = o; o = align_up(o + 4 * n);
     l.inc = o; o = align_up(o + 8 * items);
     // all-pairs scratch: packed double4 sources (EXACT) or the sorted FAST workspace
-    l.src4 = o; o = align_up(o + (fast_ws_bytes(n) > 32 * n ? fast_ws_bytes(n) : 32 * n));
+    {
+        int64_t f = fast_ws_bytes(n) > 32 * n ? fast_ws_bytes(n) : 32 * n;
+        if (p.lr_precision == BD_LR_FAST_SYM) f = sym_ws_bytes(n);
+        l.src4 = o; o = align_up(o + f);
+    }
     l.cell_id = o; o = align_up(o + (P ? 4 * n : 0));
     l.cell_start = o; o = align_up(o + (P ? 4 * (nc + 1) : 0));
     l.cell_cur = o; o = align_up(o + (P ? 4 * nc : 0));

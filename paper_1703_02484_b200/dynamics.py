@@ -18,7 +18,9 @@ Extra keyword arguments of LongRangeSimulation (not in the reference):
                composite force models of SURVEY.md §0 (Verlet-list short range
                with params.r_cutoff); the triangulation stays the overlap
                neighbour provider in every case;
-  precision    "exact" (bit-identical to the reference) or "fast" (sorted,
+  precision    "exact" (bit-identical to the reference), "fast-sym" (FAST
+               arithmetic, each unordered pair's r^-3 evaluated once for both
+               directions; single GPU; workspace ~ n^2/32 bytes) or "fast" (sorted,
                FMA + rsqrt all-pairs; |dF|/|F| ~1e-13);
   skin         Verlet skin for the short-range force (default sigma / 2).
 """
@@ -40,7 +42,7 @@ from .triangulation import TRI_KEYS, PeriodicTriangulation
 RESOLVE_FRAC = 1.0 - 1e-9  # dynamics.py:39
 
 FORCE_MODES = {"long-range": _abi.BD_FORCE_LR, "short-range": _abi.BD_FORCE_SR, "long+short": _abi.BD_FORCE_LRSR}
-PRECISIONS = {"exact": _abi.BD_LR_EXACT, "fast": _abi.BD_LR_FAST}
+PRECISIONS = {"exact": _abi.BD_LR_EXACT, "fast": _abi.BD_LR_FAST, "fast-sym": _abi.BD_LR_FAST_SYM}
 
 
 @dataclass
@@ -355,6 +357,8 @@ class LongRangeSimulation(_SimulationBase):
             raise BrownsimError("short-range force requires params.r_cutoff")
         if precision not in PRECISIONS:
             raise BrownsimError(f"unknown precision {precision!r}; have {sorted(PRECISIONS)}")
+        if precision == "fast-sym" and sharding is not None and sharding.world > 1:
+            raise BrownsimError("precision 'fast-sym' is single-GPU; the sharded force uses 'fast' or 'exact'")
         self.force_model = force
         self.precision = precision
         self.skin = 0.5 * params.sigma if skin is None else float(skin)

@@ -41,8 +41,9 @@ def long_range_kernel(pos, alpha, mu, L, tile=32, precision="exact"):
     n = pos_t.shape[0]
     out = torch.empty((n, 2), dtype=torch.float64, device=pos_t.device)
     err = torch.empty(n, dtype=torch.int64, device=pos_t.device)
-    work = torch.empty(lib().bd_long_range_workspace_bytes(n) // 8 + 8, dtype=torch.int64, device=pos_t.device)
-    prec = _abi.BD_LR_FAST if precision == "fast" else _abi.BD_LR_EXACT
+    prec = {"exact": _abi.BD_LR_EXACT, "fast": _abi.BD_LR_FAST, "fast-sym": _abi.BD_LR_FAST_SYM}[precision]
+    work = torch.empty(lib().bd_long_range_workspace_bytes_for(n, prec) // 8 + 8, dtype=torch.int64,
+                       device=pos_t.device)
     check(lib().bd_long_range_forces(pos_t.data_ptr(), a_t.data_ptr(), m_t.data_ptr(), n, float(L), 0, n, prec,
                                      out.data_ptr(), err.data_ptr(), work.data_ptr(), _stream()),
           "bd_long_range_forces")

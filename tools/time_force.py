@@ -17,9 +17,9 @@ for spec in sys.argv[1:] or ["131072:fast"]:
     mu = torch.from_numpy(np.where(t == 0, 3.0, -1.5)).cuda()
     out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
     err = torch.empty(n, dtype=torch.int64, device="cuda")
-    work = torch.empty(lib().bd_long_range_workspace_bytes(n) // 8 + 8, dtype=torch.int64, device="cuda")
+    work = torch.empty(lib().bd_long_range_workspace_bytes_for(n, {"exact": 0, "fast": 1, "fast-sym": 2}[prec]) // 8 + 8, dtype=torch.int64, device="cuda")
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    p = 1 if prec == "fast" else 0
+    p = {"exact": 0, "fast": 1, "fast-sym": 2}[prec]
     call = lambda: lib().bd_long_range_forces(pos.data_ptr(), alpha.data_ptr(), mu.data_ptr(), n, L, 0, n, p,
                                              out.data_ptr(), err.data_ptr(), work.data_ptr(), st)
     for _ in range(2):
