@@ -48,7 +48,7 @@ struct alignas(16) SelS {  // receiver image selector (axis_select of both axes)
 
 constexpr int SY_BT = 256;  // receivers per block = threads per CTA
 constexpr int SY_NW = SY_BT / 32;
-constexpr int SY_TS = 128;  // sources per shared-memory stage
+constexpr int SY_TS = 256;  // sources per shared-memory stage
 constexpr int SY_S = 8;     // chunks of the circulant distance range (grid.y)
 
 BD_HD int64_t sym_blocks(int64_t n) { return (n + SY_BT - 1) / SY_BT; }
@@ -247,27 +247,19 @@ BD_DEV void sym_diag(SymRecv& r, const SrcS& s, int64_t k, const int64_t* slot, 
     }
 }
 
-// transposed warp reduction of 8 per-lane values (one per source): after
-// it, lanes with bits (4,3,2) = g hold the warp sum of value g.  9 shuffles
-// and 9 adds for 8 sums (a butterfly per value: 40 and 40)
-BD_DEV double tree8(const double v[8], int lane) {
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+// Transposed warp reduction of 8 per-lane values, one per source, without
+// selects: lane l holds in v[u] the partial of source u ^ g(l),
+// g(l) = (l >> 2) & 7 (the pair loop visits the sources in that order), so
+// each halving step exchanges a fixed register half.  After it, lane l holds
+// the warp sum for source g(l).  9 shuffles + 9 adds for 8 sums (a
+// butterfly per value: 40 + 40).
+BD_DEV double tree8(const double v[8]) {
     double h[4], q[2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const double send = b4 ? v[j] : v[j + 4];
-        const double keep = b4 ? v[j + 4] : v[j];
-        h[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
+    for (int j = 0; j < 4; ++j) h[j] = v[j] + __shfl_xor_sync(0xffffffffu, v[j + 4], 16);
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const double send = b3 ? h[j] : h[j + 2];
-        const double keep = b3 ? h[j + 2] : h[j];
-        q[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    const double send = b2 ? q[0] : q[1];
-    const double keep = b2 ? q[1] : q[0];
-    double r = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    for (int j = 0; j < 2; ++j) q[j] = h[j] + __shfl_xor_sync(0xffffffffu, h[j + 2], 8);
+    double r = q[0] + __shfl_xor_sync(0xffffffffu, q[1], 4);
     r += __shfl_xor_sync(0xffffffffu, r, 2);
     r += __shfl_xor_sync(0xffffffffu, r, 1);
     return r;
@@ -286,13 +278,14 @@ template <int MODE>
 BD_DEV void sym_tile(SymRecv& r, const SrcS* sm, int cnt, const double* cx, const double* cy, const double* Ll,
                      double* bws, int lane) {
     int j = 0;
+    const int g = (lane >> 2) & 7;  // this lane visits source j + (u ^ g) at step u
     for (; j + SY_G <= cnt; j += SY_G) {
         double bx[SY_G], by[SY_G];
 #pragma unroll
-        for (int u = 0; u < SY_G; ++u) sym_pair<MODE>(r, sm[j + u], cx, cy, Ll, bx[u], by[u]);
-        const double sx = tree8(bx, lane), sy = tree8(by, lane);
+        for (int u = 0; u < SY_G; ++u) sym_pair<MODE>(r, sm[j + (u ^ g)], cx, cy, Ll, bx[u], by[u]);
+        const double sx = tree8(bx), sy = tree8(by);
         if ((lane & 3) == 0) {
-            const int k = j + (lane >> 2);
+            const int k = j + g;
             bws[2 * k] = sx;
             bws[2 * k + 1] = sy;
         }

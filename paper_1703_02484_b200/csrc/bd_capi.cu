@@ -321,6 +321,7 @@ void init_device_info() {
         g_lr_blocks_per_sm[1] = occupancy((const void*)k_allpairs<true>, LR_BT);
         g_lr_blocks_per_sm[0] = occupancy((const void*)k_allpairs<false>, LR_BT);
         g_fast_blocks_per_sm = occupancy((const void*)k_allpairs_fast, FS_BT);
+        cudaFuncSetAttribute((const void*)k_allpairs_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, SY_SMEM);
     });
 }
 
@@ -412,6 +413,7 @@ int launch_fast_finish(const double* pos, int64_t n, const bd_params_t& p, const
 // FAST-SYM (single GPU): sort, pack, symmetric pair kernel, combine, unsort
 int launch_sym(const double* pos, const double* alpha, const double* mu, int64_t n, const bd_params_t& p,
                const SymWs& w, double* out, int64_t* err, cudaStream_t st) {
+    init_device_info();
     if (n <= 0) return 0;
     const int64_t nc = fast_ncells(n);
     cudaError_t e = cudaMemsetAsync(w.sort.cell_off, 0, sizeof(int32_t) * (nc + 1), st);
