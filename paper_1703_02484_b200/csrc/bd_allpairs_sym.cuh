@@ -49,7 +49,13 @@ struct alignas(16) SelS {  // receiver image selector (axis_select of both axes)
 constexpr int SY_BT = 256;  // receivers per block = threads per CTA
 constexpr int SY_NW = SY_BT / 32;
 constexpr int SY_TS = 256;  // sources per shared-memory stage
-constexpr int SY_S = 8;     // chunks of the circulant distance range (grid.y)
+#ifndef BD_SY_S
+#define BD_SY_S 16
+#endif
+#ifndef BD_SY_MINB
+#define BD_SY_MINB 4
+#endif
+constexpr int SY_S = BD_SY_S;  // chunks of the circulant distance range (grid.y)
 
 BD_HD int64_t sym_blocks(int64_t n) { return (n + SY_BT - 1) / SY_BT; }
 BD_HD int64_t sym_D(int64_t n) { return sym_blocks(n) / 2; }
@@ -170,7 +176,7 @@ struct SymRecv {
     double ax[SY_R], ay[SY_R];  // receiver-side accumulators A
 };
 
-enum { SY_UNIFORM = 0, SY_SELECT = 1, SY_GENERIC = 2 };
+enum { SY_UNIFORM = 0, SY_SELECT = 1, SY_EDGE_M = 2, SY_GENERIC = 3 };
 
 // raw receiver coordinate from its selector: one of the two shifted copies is unshifted
 BD_DEV double raw_coord(double c_le, double c_gt, double L) { return c_gt < L ? c_gt : c_le; }
@@ -180,50 +186,62 @@ BD_DEV double raw_coord(double c_le, double c_gt, double L) { return c_gt < L ? 
 // d_src is minus the source's OWN minimum-image displacement to the
 // receiver; it equals d except at image ties (fl(d / L) within ulps of
 // +-1/2, e.g. lattice pairs exactly L/2 apart), where the reference's two
-// directions do not use mirror images.  Such pairs need a source within a
-// few ulps of the receiver's breakpoint, so:
-//   UNIFORM -- every source of the tile is more than SY_EDGE ulps from every
-//              breakpoint: one image shift per receiver, d_src = d;
-//   SELECT  -- per-pair image from the breakpoints (integer compares) and
-//              d_src from the exact min-image arithmetic of the source side;
+// directions do not use mirror images.  Such pairs have the source within
+// ~ulps(L) of the receiver's breakpoint value, so per (warp, tile):
+//   UNIFORM -- no breakpoint inside or near the tile's box: one image shift
+//              per receiver, d_src = d;
+//   SELECT  -- a breakpoint inside the box, none near a source: per-pair
+//              image from the breakpoints (integer compares), d_src = d;
+//   EDGE    -- a breakpoint within eps of the box: per-pair image and d_src
+//              from the exact min-image arithmetic of the source side;
 //   GENERIC -- exact min-image arithmetic on both sides (receivers within
 //              ulps of L/2 have ambiguous breakpoints; essentially never).
-constexpr uint64_t SY_EDGE = 64;
 
 template <int MODE>
 BD_DEV void sym_pair(SymRecv& r, const SrcS& s, const double* cx, const double* cy, const double* Ll, double& bx,
                      double& by) {
+    double dx[SY_R], dy[SY_R];
+#pragma unroll
+    for (int m = 0; m < SY_R; ++m) {
+        if (MODE == SY_UNIFORM) {
+            dx[m] = cx[m] - s.x;
+            dy[m] = cy[m] - s.y;
+        } else if (MODE == SY_GENERIC) {
+            dx[m] = mi_fast(raw_coord(r.cx_le[m], r.cx_gt[m], Ll[0]) - s.x, Ll[0], Ll[1], Ll[2]);
+            dy[m] = mi_fast(raw_coord(r.cy_le[m], r.cy_gt[m], Ll[0]) - s.y, Ll[0], Ll[1], Ll[2]);
+        } else {
+            dx[m] = (dbits(s.x) <= r.Tx[m] ? r.cx_le[m] : r.cx_gt[m]) - s.x;
+            dy[m] = (dbits(s.y) <= r.Ty[m] ? r.cy_le[m] : r.cy_gt[m]) - s.y;
+        }
+    }
     bx = 0.0;
     by = 0.0;
 #pragma unroll
     for (int m = 0; m < SY_R; ++m) {
-        double dx, dy, sx_, sy_;
-        if (MODE == SY_UNIFORM) {
-            dx = cx[m] - s.x;
-            dy = cy[m] - s.y;
-            sx_ = dx;
-            sy_ = dy;
-        } else {
-            const double xr = raw_coord(r.cx_le[m], r.cx_gt[m], Ll[0]);
-            const double yr = raw_coord(r.cy_le[m], r.cy_gt[m], Ll[0]);
-            if (MODE == SY_GENERIC) {
-                dx = mi_fast(xr - s.x, Ll[0], Ll[1], Ll[2]);
-                dy = mi_fast(yr - s.y, Ll[0], Ll[1], Ll[2]);
-            } else {
-                dx = (dbits(s.x) <= r.Tx[m] ? r.cx_le[m] : r.cx_gt[m]) - s.x;
-                dy = (dbits(s.y) <= r.Ty[m] ? r.cy_le[m] : r.cy_gt[m]) - s.y;
-            }
-            sx_ = -mi_fast(s.x - xr, Ll[0], Ll[1], Ll[2]);
-            sy_ = -mi_fast(s.y - yr, Ll[0], Ll[1], Ll[2]);
+        double sxm = dx[m], sym = dy[m];
+        if (MODE == SY_EDGE_M || MODE == SY_GENERIC) {  // the source side's own exact image
+            sxm = -mi_fast(s.x - raw_coord(r.cx_le[m], r.cx_gt[m], Ll[0]), Ll[0], Ll[1], Ll[2]);
+            sym = -mi_fast(s.y - raw_coord(r.cy_le[m], r.cy_gt[m], Ll[0]), Ll[0], Ll[1], Ll[2]);
         }
-        const double w = inv_r3(fma(dx, dx, dy * dy));
+        const double w = inv_r3(fma(dx[m], dx[m], dy[m] * dy[m]));
         const double ta = s.a * w;
-        r.ax[m] = fma(ta, dx, r.ax[m]);
-        r.ay[m] = fma(ta, dy, r.ay[m]);
+        r.ax[m] = fma(ta, dx[m], r.ax[m]);
+        r.ay[m] = fma(ta, dy[m], r.ay[m]);
         const double tb = r.a[m] * w;
-        bx = fma(tb, sx_, bx);
-        by = fma(tb, sy_, by);
+        bx = fma(tb, sxm, bx);
+        by = fma(tb, sym, by);
     }
+}
+
+// Does [b0, b1] (source coordinate bits) come within eps (absolute) of the
+// breakpoint T?  Image ties need |fl(x_i - s)| within ulps(L) of L/2, i.e. s
+// within ~ulps(L) of the breakpoint VALUE (a bit-pattern distance would be
+// wrong for small s).  T = ~0: no breakpoint, no tie.
+BD_DEV bool near_window(uint64_t b0, uint64_t b1, uint64_t T, double eps) {
+    if (T == ~0ull) return false;
+    const double tv = bits_to_double(T);
+    const uint64_t lo = dbits(tv - eps > 0.0 ? tv - eps : 0.0), hi = dbits(tv + eps);
+    return !(b1 < lo || b0 > hi);
 }
 
 // diagonal block (J == I): directed, receiver side only, k != i
@@ -316,7 +334,7 @@ constexpr int SY_NW2 = SY_CT / 32;   // warps per CTA
 constexpr int SY_SMEM = 2 * SY_TS * (int)sizeof(SrcS) + 2 * SY_NW2 * SY_TS * 16;
 
 // grid (Mb, SY_S), SY_CT threads; warp v of block I owns slots I*SY_BT + 64 v + {lane, lane + 32}
-__global__ void __launch_bounds__(SY_CT, 4) k_allpairs_sym(SymWs w, int64_t n, double L, double lo, double hi) {
+__global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int64_t n, double L, double lo, double hi) {
     extern __shared__ __align__(128) unsigned char sy_smem[];
     SrcS* tiles = reinterpret_cast<SrcS*>(sy_smem);                              // [2][SY_TS]
     double* bw = reinterpret_cast<double*>(sy_smem + 2 * SY_TS * sizeof(SrcS));  // [2][SY_NW2][SY_TS][2]
@@ -382,16 +400,17 @@ __global__ void __launch_bounds__(SY_CT, 4) k_allpairs_sym(SymWs w, int64_t n, d
         double* bws = bw + ((size_t)st * SY_NW2 + wid) * SY_TS * 2;
         if (use) {
             double cx[SY_R], cy[SY_R];
-            bool uni = true;
+            bool uni = true, edge = false;
+            const double eps = L * 0x1p-44;  // >> the ulps of L in which image ties live
 #pragma unroll
             for (int m = 0; m < SY_R; ++m) {
-                // every source more than SY_EDGE ulps below / above the breakpoint (no image ties)
-                const bool xle = bx1 + SY_EDGE <= r.Tx[m], xgt = bx0 > r.Tx[m] + SY_EDGE;
-                const bool yle = by1 + SY_EDGE <= r.Ty[m], ygt = by0 > r.Ty[m] + SY_EDGE;
+                const bool xle = bx1 <= r.Tx[m], xgt = bx0 > r.Tx[m], yle = by1 <= r.Ty[m], ygt = by0 > r.Ty[m];
                 uni &= (xle || xgt) && (yle || ygt);
+                edge |= near_window(bx0, bx1, r.Tx[m], eps) || near_window(by0, by1, r.Ty[m], eps);
                 cx[m] = xle ? r.cx_le[m] : r.cx_gt[m];
                 cy[m] = yle ? r.cy_le[m] : r.cy_gt[m];
             }
+            const bool any_edge = __any_sync(0xffffffffu, edge);
             const bool all_uni = __all_sync(0xffffffffu, uni);
             if (d == 0) {
                 if (wamb) {
@@ -401,6 +420,8 @@ __global__ void __launch_bounds__(SY_CT, 4) k_allpairs_sym(SymWs w, int64_t n, d
                 }
             } else if (wamb) {
                 sym_tile<SY_GENERIC>(r, sm, cnt, cx, cy, Ll, bws, lane);
+            } else if (any_edge) {
+                sym_tile<SY_EDGE_M>(r, sm, cnt, cx, cy, Ll, bws, lane);
             } else if (all_uni) {
                 sym_tile<SY_UNIFORM>(r, sm, cnt, cx, cy, Ll, bws, lane);
             } else {

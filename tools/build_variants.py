@@ -9,14 +9,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1703_02484_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "inline_sel": ["BD_FS_INLINE_SEL=1"],
-    "inline_sel_ts256_s2": ["BD_FS_INLINE_SEL=1", "BD_FS_TS=256", "BD_FS_S=2"],
-    "bt128_ts128_s4": ["BD_FS_BT=128", "BD_FS_TS=128", "BD_FS_S=4"],
-    "bt128_ts256_s2": ["BD_FS_BT=128", "BD_FS_TS=256", "BD_FS_S=2"],
-    "bt256_ts256_s4": ["BD_FS_BT=256", "BD_FS_TS=256", "BD_FS_S=4"],
-    "bt256_ts256_s3": ["BD_FS_BT=256", "BD_FS_TS=256", "BD_FS_S=3"],
-    "bt256_ts128_s4": ["BD_FS_BT=256", "BD_FS_TS=128", "BD_FS_S=4"],
-    "bt512_ts256_s4": ["BD_FS_BT=512", "BD_FS_TS=256", "BD_FS_S=4"],
+    "sym_minb3": ["BD_SY_MINB=3"],
+    "sym_minb5": ["BD_SY_MINB=5"],
+    "sym_s4": ["BD_SY_S=4"],
+    "sym_s16": ["BD_SY_S=16"],
 }
 
 if __name__ == "__main__":
