@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=131072)
     ap.add_argument("--rho", type=float, default=0.3)
-    ap.add_argument("--precision", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "fast-sym", "fast", "exact"],
+                    help="auto: fast-sym on one GPU (Newton's third law on r^-3), fast when sharded")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -193,6 +194,8 @@ def run_ours(args):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
     n = args.n
+    if args.precision == "auto":
+        args.precision = "fast-sym" if world == 1 else "fast"
     box, pos, types, alpha, mu = workload(n, args.rho)
     t_setup = time.perf_counter()
     sys_ = ParticleSystem(pos, types, alpha, mu, box)
@@ -300,8 +303,11 @@ def run_ours(args):
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "particle-steps/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {exc}"}
-    traffic = profiled_traffic("k_allpairs_fast" if args.precision == "fast" else "k_allpairs")
-    launches_per_step = (9 if args.precision == "fast" else 3) if world == 1 else (9 if args.precision == "fast" else 4)
+    kname = {"fast-sym": "k_allpairs_sym", "fast": "k_allpairs_fast", "exact": "k_allpairs"}[args.precision]
+    traffic, pipe = profiled_traffic(kname)
+    # kernels of ours per step: sort (4) + pack + pair kernel + combine/reduce + unsort + rescan, then the
+    # persistent step kernel (fast / fast-sym); pack + pair kernel + step kernel (exact); +2 slot copies sharded
+    launches_per_step = (10 if args.precision != "exact" else 3) + (0 if world == 1 or args.precision != "exact" else 2)
     line = {
         "metric": "particle-steps/s (N x steps / s), long-range all-pairs + Delaunay maintenance + overlap correction",
         "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -319,10 +325,14 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": "measured DFMA probe on this GPU (bd_probe_fp64)" if fp64
                      else "nominal 148x64x2x1.965GHz",
-                     "kernel": "k_allpairs_fast" if args.precision == "fast" else "k_allpairs<EXACT>",
-                     "flops_per_pair": FLOPS_PER_PAIR,
-                     "note": "compute-bound FP64 kernel; traffic = DRAM bytes per launch from the committed "
-                             "ncu --set full capture (profiles/)"},
+                     "kernel": kname, "flops_per_pair": FLOPS_PER_PAIR,
+                     "fp64_pipe_active_pct_ncu": pipe,
+                     "note": "compute-bound FP64 kernel; achieved = 23 algorithmic flops per DIRECTED pair "
+                             "(the reference's arithmetic) over the device time of the whole force phase (sort, "
+                             "pack, pair kernel, combine); fast-sym executes 8 FP64 instructions per directed "
+                             "pair (one r^-3 per unordered pair) so the pipe utilisation from ncu is the "
+                             "hardware-side figure; traffic = DRAM bytes per launch of the pair kernel from the "
+                             "committed ncu --set full capture (profiles/)"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": K * launches_per_step,
@@ -345,18 +355,18 @@ def sys_first_forces(n, pos, alpha, mu, box):
 
 
 def profiled_traffic(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_full_k_allpairs_fast.json")
+    """(dram bytes per launch, fp64 pipe %) of `kernel` from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", f"r01_ncu_full_{kernel}.json")
     try:
         for d in json.load(open(path)):
             if kernel in d["kernel"]:
                 def mb(v):
                     num, unit = v.split()
                     return float(num) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
-                return mb(d["dram_read"]) + mb(d["dram_write"])
+                return mb(d["dram_read"]) + mb(d["dram_write"]), float(d["fp64_pipe_pct"].split()[0])
     except Exception:
-        return None
-    return None
+        return None, None
+    return None, None
 
 
 def run_reference(args):

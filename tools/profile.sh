@@ -8,8 +8,11 @@ timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none --
 # full capture of the FAST all-pairs kernel (N = 131,072)
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:k_allpairs_fast -s 1 -c 1 \
     -o gpurun_out/prof_allpairs_fast python tools/prof_force.py 131072 fast 2 > gpurun_out/ncu_ap.log 2>&1
+# full capture of the FAST-SYM pair kernel (N = 131,072; the bench default on one GPU)
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:k_allpairs_sym -s 1 -c 1 \
+    -o gpurun_out/prof_allpairs_sym python tools/prof_force.py 131072 fast-sym 2 > gpurun_out/ncu_aps.log 2>&1
 # full capture of the EXACT all-pairs kernel (N = 131,072)
-timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:"k_allpairs<0" -c 1 \
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k k_allpairs -c 1 \
     -o gpurun_out/prof_allpairs_exact python tools/prof_force.py 131072 exact 1 > gpurun_out/ncu_apx.log 2>&1
 # full capture of the persistent step kernel (cfg3 state after warm-up)
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_step_tri_grid -s 2 -c 1 \
