@@ -46,14 +46,18 @@ struct alignas(16) SelS {  // receiver image selector (axis_select of both axes)
     uint64_t Tx, Ty, amb, pad;
 };
 
-constexpr int SY_BT = 256;  // receivers per block = threads per CTA
-constexpr int SY_NW = SY_BT / 32;
+#ifndef BD_SY_CT
+#define BD_SY_CT 256
+#endif
+constexpr int SY_R = 2;                // receivers per lane
+constexpr int SY_CT = BD_SY_CT;        // threads per CTA
+constexpr int SY_BT = SY_CT * SY_R;    // receivers per block
 constexpr int SY_TS = 256;  // sources per shared-memory stage
 #ifndef BD_SY_S
-#define BD_SY_S 16
+#define BD_SY_S 32
 #endif
 #ifndef BD_SY_MINB
-#define BD_SY_MINB 4
+#define BD_SY_MINB 2
 #endif
 constexpr int SY_S = BD_SY_S;  // chunks of the circulant distance range (grid.y)
 
@@ -167,8 +171,6 @@ BD_DEV double inv_r3(double r2) {
 // every source read from shared memory feeds two pair evaluations, and the
 // source-side partial of a lane is the sum over its two receivers before
 // the warp butterfly (so the reduction is amortised over 64 pairs).
-constexpr int SY_R = 2;
-
 struct SymRecv {
     double cx_le[SY_R], cx_gt[SY_R], cy_le[SY_R], cy_gt[SY_R];
     uint64_t Tx[SY_R], Ty[SY_R];
@@ -328,7 +330,6 @@ BD_DEV void sym_issue(const SymWs& w, int64_t n, int64_t t, SrcS* tiles, uint64_
     if (cnt) bulk_g2s(tiles + st * SY_TS, w.src + t * SY_TS, (uint32_t)(cnt * sizeof(SrcS)), &bars[st]);
 }
 
-constexpr int SY_CT = SY_BT / SY_R;  // threads per CTA
 constexpr int SY_NW2 = SY_CT / 32;   // warps per CTA
 // dynamic smem: 2 source stages + 2 buffers of per-warp source-side sums
 constexpr int SY_SMEM = 2 * SY_TS * (int)sizeof(SrcS) + 2 * SY_NW2 * SY_TS * 16;

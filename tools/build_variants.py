@@ -9,10 +9,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1703_02484_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "sym_minb3": ["BD_SY_MINB=3"],
-    "sym_minb5": ["BD_SY_MINB=5"],
-    "sym_s4": ["BD_SY_S=4"],
-    "sym_s16": ["BD_SY_S=16"],
+    "sym_ct256_minb2": ["BD_SY_CT=256", "BD_SY_MINB=2"],
+    "sym_ct256_minb2_s32": ["BD_SY_CT=256", "BD_SY_MINB=2", "BD_SY_S=32"],
+    "sym_s32": ["BD_SY_S=32"],
 }
 
 if __name__ == "__main__":
