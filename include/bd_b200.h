@@ -92,6 +92,13 @@ typedef struct bd_stats {
     int64_t status, err_i, err_k;
     int64_t rebuilds; /* Verlet rebuilds during this step */
     int64_t reserved[6];
+    /* device work of the step, for the algorithmic-bytes roofline of the
+     * O(N) path: passes of integrate, apply_crossings,
+     * edge-inversion check, per-edge flag passes, per-triangle area passes,
+     * independent-set rounds, flipped edges, overlap passes, overlap
+     * gather/apply passes, incidence builds, Verlet rebuilds, short-range
+     * force evaluations, then 4 spare words */
+    int64_t work[16];
 } bd_stats_t;
 
 /* device state of one simulation */

@@ -163,6 +163,7 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
         out->status = (int64_t)c.w.ctl->status;
         out->err_i = (int64_t)c.w.ctl->err_i;
         out->err_k = (int64_t)c.w.ctl->err_k;
+        for (int k = 0; k < WK_N; ++k) out->work[k] = c.work[k];
         *c.s.call = c.call;
     }
 }
@@ -176,7 +177,7 @@ BD_HD int64_t overlap_rounds(X& x, Red<X>& R, Ctx& c, double margin) {
     int64_t iters = 0, round;
     for (round = 0; round < c.p.max_overlap_iters; ++round) {
         const SubsetPairs sp{c.s.pair_a, c.s.pair_b, c.w.ov_idx, (int64_t)x.ld((const u64*)&c.s.vl_meta[3])};
-        build_incidence(x, c.p.n, sp, c.w.inc_off, c.w.inc_cur, c.w.inc);
+        build_incidence(x, c.p.n, sp, c.w.inc_off, c.w.inc_cur, c.w.inc, c.work);
         const int64_t ri = correct_overlaps(x, R, c, sp, false);
         if (ri < 0) break;
         iters += ri;
@@ -206,6 +207,7 @@ BD_HD void verlet_stats(X& x, Red<X>& R, Ctx& c, bd_stats_t* out, int64_t rebuil
         out->status = (int64_t)c.w.ctl->status;
         out->err_i = (int64_t)c.w.ctl->err_i;
         out->err_k = (int64_t)c.w.ctl->err_k;
+        for (int k = 0; k < WK_N; ++k) out->work[k] = c.work[k];
         *c.s.call = c.call;
     }
 }

@@ -121,12 +121,36 @@ BD_HD Ws ws_carve(void* base, const bd_params_t& p, int64_t ne, int64_t nt) {
     return w;
 }
 
+// Work counters of one step (uniform across threads: every thread runs the
+// same phase sequence), reported in bd_stats_t.work[] so the host can turn
+// them into algorithmic bytes (bench.py "maintain_roofline").
+enum {
+    WK_INTEGRATE = 0,  // integrate passes (attempts)
+    WK_APPLY_CROSS,    // apply_crossings passes
+    WK_EDGE_INV,       // edge-inversion (pass-through) checks
+    WK_FLAG_PASS,      // per-edge predicate passes (in-circle / inversion flags)
+    WK_AREA_PASS,      // per-triangle signed-area passes
+    WK_LFMIS_ROUND,    // independent-set selection rounds
+    WK_FLIPS,          // edges flipped
+    WK_OVL_PASS,       // overlap passes over the pair list (incl. the final clean one)
+    WK_OVL_APPLY,      // overlap gather/apply passes
+    WK_INCIDENCE,      // incidence-list builds
+    WK_VL_REBUILD,     // Verlet list rebuilds
+    WK_SR_FORCE,       // short-range force evaluations
+    WK_N
+};
+
 struct Ctx {
     bd_params_t p;
     bd_state_t s;
     Ws w;
     uint64_t call;
+    int64_t work[WK_N];
 };
+
+BD_HD void ctx_init_work(Ctx& c) {
+    for (int k = 0; k < WK_N; ++k) c.work[k] = 0;
+}
 
 template <class X>
 BD_HD void set_error(X& x, Ctx& c, u64 code, int64_t i, int64_t k) {
@@ -254,6 +278,7 @@ BD_HD void ph_tri_copy(X& x, const bd_tri_t& a, bd_tri_t& b) {
 // integrate (dynamics.py:73-94) fused with the crossing bookkeeping; returns #particles that crossed
 template <class X>
 BD_HD u64 ph_integrate(X& x, Red<X>& R, Ctx& c, double dt, int64_t* cross64 = nullptr) {
+    c.work[WK_INTEGRATE]++;
     u64* r = R.open();
     const double L = c.p.L, scale = sqrt(c.p.diffusion * dt), clamp = c.p.clamp;
     double* pos = c.s.pos;
@@ -282,6 +307,7 @@ BD_HD u64 ph_integrate(X& x, Red<X>& R, Ctx& c, double dt, int64_t* cross64 = nu
 // apply_crossings (triangulation.py:166-177), only called when some particle crossed
 template <class X>
 BD_HD void ph_apply_crossings(X& x, Ctx& c) {
+    c.work[WK_APPLY_CROSS]++;
     bd_tri_t& T = c.s.tri;
     for (int64_t t = x.tid(); t < T.nt; t += x.nth()) {
         int32_t ts[3][2];
@@ -297,6 +323,7 @@ BD_HD void ph_apply_crossings(X& x, Ctx& c) {
 // edge_inversion_present (triangulation.py:240-250)
 template <class X>
 BD_HD bool ph_edge_inversion(X& x, Red<X>& R, Ctx& c) {
+    c.work[WK_EDGE_INV]++;
     u64* r = R.open();
     const bd_tri_t& T = c.s.tri;
     const double* prev = c.s.prev;
@@ -313,6 +340,7 @@ BD_HD bool ph_edge_inversion(X& x, Red<X>& R, Ctx& c) {
 // signed_area2 <= 0 per triangle; returns #inverted
 template <class X>
 BD_HD u64 ph_inverted_tris(X& x, Red<X>& R, Ctx& c) {
+    c.work[WK_AREA_PASS]++;
     u64* r = R.open();
     const bd_tri_t& T = c.s.tri;
     for (int64_t t = x.tid(); t < T.nt; t += x.nth()) {
@@ -336,6 +364,7 @@ BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c) {
     uint8_t* st = c.w.estat;
     u64 nsel_total = 0;
     for (;;) {
+        c.work[WK_LFMIS_ROUND]++;
         u64* rs = R.open();
         for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
             if (st[e] != ES_UND) continue;
@@ -377,6 +406,7 @@ BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c) {
         if (R.close(ru) == 0) break;
     }
     if (nsel_total == 0) return 0;
+    c.work[WK_FLIPS] += (int64_t)nsel_total;
     for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
         if (st[e] != ES_SEL) continue;
         const int rc = flip_edge(T, e);
@@ -392,6 +422,7 @@ BD_HD int64_t restore_delaunay(X& x, Red<X>& R, Ctx& c, int64_t max_passes) {
     bd_tri_t& T = c.s.tri;
     int64_t passes = 0;
     for (;;) {
+        c.work[WK_FLAG_PASS]++;
         u64* r = R.open();
         for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
             V2 q[4];
@@ -423,6 +454,7 @@ BD_HD int repair_inversions(X& x, Red<X>& R, Ctx& c, int64_t max_passes, int64_t
     for (int64_t pass = 0; pass < max_passes; ++pass) {
         if (passes) *passes = pass;
         if (ph_inverted_tris(x, R, c) == 0) return 0;
+        c.work[WK_FLAG_PASS]++;
         for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
             V2 q[4];
             edge_quad(T, c.s.pos, c.p.L, e, q);
@@ -489,7 +521,9 @@ struct SubsetPairs {
 // vertex -> incident pairs, ascending pair index (fixes the reference's
 // ascending-pair accumulation order of overlap_pass_kernel / short_range_kernel)
 template <class X, class PS>
-BD_HD void build_incidence(X& x, int64_t n, const PS& ps, int32_t* off, int32_t* cur, int32_t* inc) {
+BD_HD void build_incidence(X& x, int64_t n, const PS& ps, int32_t* off, int32_t* cur, int32_t* inc,
+                           int64_t* work = nullptr) {
+    if (work) work[WK_INCIDENCE]++;
     for (int64_t i = x.tid(); i < n; i += x.nth()) {
         off[i] = 0;
         cur[i] = 0;
@@ -527,7 +561,7 @@ BD_HD void build_incidence(X& x, int64_t n, const PS& ps, int32_t* off, int32_t*
 template <class X>
 BD_HD void build_edge_incidence(X& x, Ctx& c) {
     const EdgePairs ps{c.s.tri.edge_v, c.s.tri.ne};
-    build_incidence(x, c.p.n, ps, c.w.inc_off, c.w.inc_cur, c.w.inc);
+    build_incidence(x, c.p.n, ps, c.w.inc_off, c.w.inc_cur, c.w.inc, c.work);
 }
 
 // correct_overlaps (dynamics.py:97-133) over a fixed pair set with its
@@ -540,6 +574,7 @@ BD_HD int64_t correct_overlaps(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri) 
     const int64_t m = ps.count();
     int64_t iterations = 0;
     for (int64_t it = 0; it < c.p.max_overlap_iters; ++it) {
+        c.work[WK_OVL_PASS]++;
         u64* r = R.open();
         for (int64_t e = x.tid(); e < m; e += x.nth()) {
             const int64_t a = ps.a(e), b = ps.b(e);
@@ -557,6 +592,7 @@ BD_HD int64_t correct_overlaps(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri) 
         }
         if (R.close(r) == 0) return iterations;
         iterations++;
+        c.work[WK_OVL_APPLY]++;
         u64* rc = R.open();
         for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
             double dx = 0.0, dy = 0.0;

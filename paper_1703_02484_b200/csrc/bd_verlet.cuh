@@ -108,6 +108,7 @@ BD_HD bool vl_stale(X& x, Red<X>& R, Ctx& c) {
 // Returns false on a capacity overflow (status BD_ERR_CAPACITY).
 template <class X>
 BD_HD bool vl_rebuild(X& x, Red<X>& R, Ctx& c, double margin) {
+    c.work[WK_VL_REBUILD]++;
     const int64_t n = c.p.n, ncx = c.p.ncx;
     int32_t* cnt = c.w.pcnt;
     int64_t rows;
@@ -171,7 +172,7 @@ BD_HD bool vl_rebuild(X& x, Red<X>& R, Ctx& c, double margin) {
     x.sync();
     // incidence of the Verlet pairs (ascending pair index per particle)
     const ListPairs lp{c.s.pair_a, c.s.pair_b, total};
-    build_incidence(x, n, lp, c.w.vinc_off, c.w.vinc_cur, c.w.vinc);
+    build_incidence(x, n, lp, c.w.vinc_off, c.w.vinc_cur, c.w.vinc, c.work);
     int64_t nov = 0;
     if (margin > 0.0) {
         // overlap candidates: pairs within margin at build time, order kept (forces.py:145-149)
@@ -203,6 +204,7 @@ BD_HD bool vl_rebuild(X& x, Red<X>& R, Ctx& c, double margin) {
 // short_range_kernel (_kernels.py:62-91) gathered per particle: out[i], err[i]
 template <class X>
 BD_HD void sr_forces(X& x, Ctx& c, double* out, int64_t* err) {
+    c.work[WK_SR_FORCE]++;
     const double rc2 = c.p.r_cut * c.p.r_cut;
     const double* pos = c.s.pos;
     for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {

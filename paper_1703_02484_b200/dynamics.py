@@ -61,6 +61,8 @@ class StepStats:
     overlap_ms: float = 0.0
     step_ms: float = 0.0
     overlap_flags: np.ndarray | None = field(default=None, repr=False)
+    # device work counters of the step (not in the reference; csrc/bd_step.cuh WK_*, roofline.py)
+    work: dict | None = field(default=None, repr=False)
 
 
 from .validation import MissedOverlapError  # noqa: E402  (dynamics.py:69-70)
@@ -218,7 +220,9 @@ def _raise_for(st: dict, step_index: int):
 
 def _decode_stats(words: np.ndarray) -> dict:
     raw = _abi.BdStats.from_buffer_copy(np.ascontiguousarray(words, dtype=np.int64).tobytes())
-    return {k: getattr(raw, k) for k, _ in _abi.BdStats._fields_ if k != "reserved"}
+    d = {k: getattr(raw, k) for k, _ in _abi.BdStats._fields_ if k not in ("reserved", "work")}
+    d["work"] = {k: int(raw.work[i]) for i, k in enumerate(_abi.WORK_KEYS)}
+    return d
 
 
 class _SimulationBase:
@@ -303,7 +307,8 @@ class _SimulationBase:
                                  inversion_repairs=st["inversion_repairs"], rollbacks=st["rollbacks"],
                                  n_overlapping=st["n_overlapping"],
                                  force_ms=force_ms if self._two_phase else 0.0,
-                                 maintain_ms=drv_ms, overlap_ms=0.0, step_ms=force_ms + drv_ms, overlap_flags=flags))
+                                 maintain_ms=drv_ms, overlap_ms=0.0, step_ms=force_ms + drv_ms, overlap_flags=flags,
+                                 work=st["work"]))
             self.step_index += 1
         return res
 

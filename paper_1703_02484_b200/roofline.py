@@ -1,0 +1,45 @@
+"""Algorithmic-byte accounting of the O(N) step (host side, for reporting).
+
+The persistent step kernels run many short memory-bound passes (integrate,
+pass-through check, flag passes, independent-set rounds, flips, overlap
+sweeps, incidence builds, Verlet rebuilds, short-range forces).  Each step
+reports how many of each it ran (bd_stats_t.work[], csrc/bd_step.cuh WK_*);
+this module turns the counts into the minimum bytes those passes must move
+(per-unit figures of SURVEY.md §8(d), N particles, E = 3N edges, F = 2N
+triangles, P stored pairs), so that bytes / step time is the achieved
+bandwidth to compare with the HBM roofline.
+"""
+
+from __future__ import annotations
+
+# bytes per pass (functions of n, ne, nt, pairs) -- SURVEY.md §8(d)
+PASS_BYTES = {
+    "integrate": lambda n, e, t, p: 64 * n,                        # r pos, r F, w prev, w pos
+    "apply_crossings": lambda n, e, t, p: 30 * t + 2 * n,          # tri_v + shifts r/w, crossings
+    "edge_inversion": lambda n, e, t, p: 8 * e + 32 * n,           # edge_v + prev/cur positions
+    "flag_pass": lambda n, e, t, p: 11 * e + 18 * t + 16 * n,      # edge quad gather + flag write
+    "area_pass": lambda n, e, t, p: 19 * t + 16 * n,               # tri_v, shifts, positions, flag
+    "lfmis_round": lambda n, e, t, p: 17 * e,                      # status of the edge + 4 neighbours
+    "flips": lambda n, e, t, p: 190,                               # per flipped edge
+    "overlap_pass": lambda n, e, t, p: 8 * max(e, p) + 32 * n,     # pair list + positions
+    "overlap_apply": lambda n, e, t, p: 25 * max(e, p) + 32 * n,   # incidence, contributions, positions r/w
+    "incidence": lambda n, e, t, p: 24 * max(e, p),                # CSR of pairs per particle
+    "verlet_rebuild": lambda n, e, t, p: 16 * n + 8 * p,
+    "sr_force": lambda n, e, t, p: 8 * p + 40 * n,
+}
+
+
+def step_bytes(work: dict, n: int, ne: int, nt: int, pairs: int = 0) -> int:
+    """Algorithmic bytes of one step from its work counters."""
+    return int(sum(PASS_BYTES[k](n, ne, nt, pairs) * int(v) for k, v in work.items() if k in PASS_BYTES))
+
+
+def hbm_peak_gbs(measured: dict, default: float = 6538.6) -> float:
+    """HBM copy bandwidth from MEASURED_PEAKS.json (driver-written), else the recipe's figure."""
+    for key in ("hbm_gbs", "hbm_copy_gbs", "hbm_burst_gbs", "hbm_GBps"):
+        if key in measured:
+            try:
+                return float(measured[key])
+            except (TypeError, ValueError):
+                pass
+    return default

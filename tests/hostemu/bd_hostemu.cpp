@@ -19,6 +19,7 @@ static Ctx host_ctx(const bd_state_t* s, const bd_params_t* p) {
     c.s = *s;
     c.w = ws_carve(s->work, *p, s->tri.ne, s->tri.nt);
     c.call = s->call ? *s->call : 0;
+    ctx_init_work(c);
     return c;
 }
 

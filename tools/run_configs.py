@@ -36,7 +36,7 @@ CFGS = {
     1: dict(n=1024, rho=0.3, force="long-range", precision="exact", steps=100, seed=0),
     2: dict(n=16384, rho=0.3, force="short-range", precision="exact", steps=100, seed=0),
     4: dict(n=1048576, rho=0.6, force="short-range", precision="exact", steps=20, seed=1),
-    5: dict(n=65536, rho=0.3, force="long+short", precision="fast", steps=10000, seed=0),
+    5: dict(n=65536, rho=0.3, force="long+short", precision="fast-sym", steps=10000, seed=0),
 }
 RESOLVE = 1.0 - 1e-9
 
@@ -105,7 +105,9 @@ def run(cfg_id, args):
     u0 = sim.sys.unwrapped_positions().clone()
     msd_t = sorted({int(round(v)) for v in np.logspace(0, np.log10(K), 25)} | {K})
     msd = []
-    dev_ms, bad, checks = 0.0, [], 0
+    from paper_1703_02484_b200.roofline import hbm_peak_gbs, step_bytes
+    dev_ms, maint_ms, mbytes, bad, checks = 0.0, 0.0, 0, [], 0
+    ne, nt = sim.tri.n_edges, sim.tri.n_triangles
     stats_tot = dict(overlap_iterations=0, flip_passes=0, inversion_repairs=0, rollbacks=0)
     done = 0
     while done < K:
@@ -117,6 +119,9 @@ def run(cfg_id, args):
         res = sim.run(chunk)
         done += chunk
         dev_ms += sum(s.step_ms for s in res)
+        maint_ms += sum(s.maintain_ms for s in res)
+        pairs = int(sim._eng.vl_meta[0].item()) if cfg["force"] != "long-range" else 0
+        mbytes += sum(step_bytes(s.work, n, ne, nt, pairs) for s in res)
         for s in res:
             for k in stats_tot:
                 stats_tot[k] += getattr(s, k)
@@ -142,6 +147,10 @@ def run(cfg_id, args):
             "ms_per_step": dev_ms / K, "valid_every_checked_step": not bad, "checks": checks,
             "check_every": every, "overlap_scan": "brute" if brute else "cell-list", "violations": bad[:5],
             "stats_total": stats_tot, "build_s": t_build, "cpu_baseline": cpu,
+            "phase_ms": {"force": (dev_ms - maint_ms) / K, "maintain": maint_ms / K},
+            "maintain_roofline": {"bound": "hbm", "achieved": mbytes / (maint_ms * 1e-3) / 1e9, "unit": "GB/s",
+                                  "peak": hbm_peak_gbs({}), "frac": mbytes / (maint_ms * 1e-3) / 1e9 / hbm_peak_gbs({}),
+                                  "bytes_per_step": mbytes / K},
             "msd": msd if cfg_id == 5 else None}
     print(json.dumps(line), flush=True)
     return line
