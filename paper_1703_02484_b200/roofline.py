@@ -12,26 +12,29 @@ bandwidth to compare with the HBM roofline.
 
 from __future__ import annotations
 
-# bytes per pass (functions of n, ne, nt, pairs) -- SURVEY.md §8(d)
+# bytes per pass -- SURVEY.md §8(d); n particles, e edges, t triangles,
+# p Verlet pairs (short-range force / list build), q overlap pairs (the
+# triangulation edges, or the Verlet overlap candidates without a triangulation)
 PASS_BYTES = {
-    "integrate": lambda n, e, t, p: 64 * n,                        # r pos, r F, w prev, w pos
-    "apply_crossings": lambda n, e, t, p: 30 * t + 2 * n,          # tri_v + shifts r/w, crossings
-    "edge_inversion": lambda n, e, t, p: 8 * e + 32 * n,           # edge_v + prev/cur positions
-    "flag_pass": lambda n, e, t, p: 11 * e + 18 * t + 16 * n,      # edge quad gather + flag write
-    "area_pass": lambda n, e, t, p: 19 * t + 16 * n,               # tri_v, shifts, positions, flag
-    "lfmis_round": lambda n, e, t, p: 17 * e,                      # status of the edge + 4 neighbours
-    "flips": lambda n, e, t, p: 190,                               # per flipped edge
-    "overlap_pass": lambda n, e, t, p: 8 * max(e, p) + 32 * n,     # pair list + positions
-    "overlap_apply": lambda n, e, t, p: 25 * max(e, p) + 32 * n,   # incidence, contributions, positions r/w
-    "incidence": lambda n, e, t, p: 24 * max(e, p),                # CSR of pairs per particle
-    "verlet_rebuild": lambda n, e, t, p: 16 * n + 8 * p,
-    "sr_force": lambda n, e, t, p: 8 * p + 40 * n,
+    "integrate": lambda n, e, t, p, q: 64 * n,                     # r pos, r F, w prev, w pos
+    "apply_crossings": lambda n, e, t, p, q: 30 * t + 2 * n,       # tri_v + shifts r/w, crossings
+    "edge_inversion": lambda n, e, t, p, q: 8 * e + 32 * n,        # edge_v + prev/cur positions
+    "flag_pass": lambda n, e, t, p, q: 11 * e + 18 * t + 16 * n,   # edge quad gather + flag write
+    "area_pass": lambda n, e, t, p, q: 19 * t + 16 * n,            # tri_v, shifts, positions, flag
+    "lfmis_round": lambda n, e, t, p, q: 17 * e,                   # status of the edge + 4 neighbours
+    "flips": lambda n, e, t, p, q: 190,                            # per flipped edge
+    "overlap_pass": lambda n, e, t, p, q: 8 * q + 32 * n,          # pair list + positions
+    "overlap_apply": lambda n, e, t, p, q: 25 * q + 32 * n,        # incidence, contributions, positions r/w
+    "incidence": lambda n, e, t, p, q: 24 * q,                     # CSR of pairs per particle
+    "verlet_rebuild": lambda n, e, t, p, q: 16 * n + 8 * p,
+    "sr_force": lambda n, e, t, p, q: 8 * p + 40 * n,
 }
 
 
-def step_bytes(work: dict, n: int, ne: int, nt: int, pairs: int = 0) -> int:
+def step_bytes(work: dict, n: int, ne: int, nt: int, pairs: int = 0, overlap_pairs: int | None = None) -> int:
     """Algorithmic bytes of one step from its work counters."""
-    return int(sum(PASS_BYTES[k](n, ne, nt, pairs) * int(v) for k, v in work.items() if k in PASS_BYTES))
+    q = ne if overlap_pairs is None else overlap_pairs
+    return int(sum(PASS_BYTES[k](n, ne, nt, pairs, q) * int(v) for k, v in work.items() if k in PASS_BYTES))
 
 
 def hbm_peak_gbs(measured: dict, default: float = 6538.6) -> float:

@@ -106,7 +106,7 @@ def run(cfg_id, args):
     msd_t = sorted({int(round(v)) for v in np.logspace(0, np.log10(K), 25)} | {K})
     msd = []
     from paper_1703_02484_b200.roofline import hbm_peak_gbs, step_bytes
-    dev_ms, maint_ms, mbytes, bad, checks = 0.0, 0.0, 0, [], 0
+    dev_ms, maint_ms, mbytes, bad, checks, work_tot = 0.0, 0.0, 0, [], 0, {}
     ne, nt = sim.tri.n_edges, sim.tri.n_triangles
     stats_tot = dict(overlap_iterations=0, flip_passes=0, inversion_repairs=0, rollbacks=0)
     done = 0
@@ -122,6 +122,9 @@ def run(cfg_id, args):
         maint_ms += sum(s.maintain_ms for s in res)
         pairs = int(sim._eng.vl_meta[0].item()) if cfg["force"] != "long-range" else 0
         mbytes += sum(step_bytes(s.work, n, ne, nt, pairs) for s in res)
+        for s_ in res:
+            for k, v in s_.work.items():
+                work_tot[k] = work_tot.get(k, 0) + v
         for s in res:
             for k in stats_tot:
                 stats_tot[k] += getattr(s, k)
@@ -148,6 +151,7 @@ def run(cfg_id, args):
             "check_every": every, "overlap_scan": "brute" if brute else "cell-list", "violations": bad[:5],
             "stats_total": stats_tot, "build_s": t_build, "cpu_baseline": cpu,
             "phase_ms": {"force": (dev_ms - maint_ms) / K, "maintain": maint_ms / K},
+            "work_per_step": {k: v / K for k, v in work_tot.items()},
             "maintain_roofline": {"bound": "hbm", "achieved": mbytes / (maint_ms * 1e-3) / 1e9, "unit": "GB/s",
                                   "peak": hbm_peak_gbs({}), "frac": mbytes / (maint_ms * 1e-3) / 1e9 / hbm_peak_gbs({}),
                                   "bytes_per_step": mbytes / K},
