@@ -18,10 +18,24 @@ using namespace bd;
 namespace {
 
 constexpr int STEP_BT = 256;
+// The persistent step kernels exist twice: at <= 128 registers (2 CTAs per SM:
+// fewer, cheaper grid barriers -- best while barrier latency dominates) and
+// at 64 registers (4 CTAs per SM: twice the memory-level parallelism for the
+// dependent gathers of large N; 25 % faster at N = 1M, slower at 16k).
+constexpr int WIDE_MINB = 4;
+int64_t wide_min_n() {  // BD_WIDE_MIN_N overrides (tests: the two variants must agree bit for bit)
+    static int64_t v = -1;
+    if (v < 0) {
+        const char* e = getenv("BD_WIDE_MIN_N");
+        v = e ? atoll(e) : 200000;
+    }
+    return v;
+}
 constexpr int BLOCK_BT = 1024;
 
 int g_num_sms = 0;
 int g_grid_blocks_per_sm = 0;
+int g_wide_blocks_per_sm = 0;
 int g_lr_blocks_per_sm[2] = {1, 1};
 int g_fast_blocks_per_sm = 1;
 std::once_flag g_once;
@@ -46,7 +60,8 @@ BD_DEV Ctx make_ctx(const bd_state_t& s, const bd_params_t& p) {
 }
 
 // ---- persistent drivers: cooperative grid (barrier = grid.sync) and one CTA
-__global__ void __launch_bounds__(STEP_BT) k_step_tri_grid(bd_state_t s, bd_params_t p, bd_stats_t* out) {
+template <int MINB>
+__global__ void __launch_bounds__(STEP_BT, MINB) k_step_tri_grid(bd_state_t s, bd_params_t p, bd_stats_t* out) {
     Ctx c = make_ctx(s, p);
     ExecGrid x{c.w.ctl};
     step_tri_after_force(x, c, out);
@@ -58,7 +73,8 @@ __global__ void __launch_bounds__(BLOCK_BT) k_step_tri_block(bd_state_t s, bd_pa
     step_tri_after_force(x, c, out);
 }
 
-__global__ void __launch_bounds__(STEP_BT) k_step_verlet_grid(bd_state_t s, bd_params_t p, bd_stats_t* out) {
+template <int MINB>
+__global__ void __launch_bounds__(STEP_BT, MINB) k_step_verlet_grid(bd_state_t s, bd_params_t p, bd_stats_t* out) {
     Ctx c = make_ctx(s, p);
     ExecGrid x{c.w.ctl};
     step_verlet(x, c, out);
@@ -70,7 +86,8 @@ __global__ void __launch_bounds__(BLOCK_BT) k_step_verlet_block(bd_state_t s, bd
     step_verlet(x, c, out);
 }
 
-__global__ void __launch_bounds__(STEP_BT) k_step_abp_grid(bd_state_t s, bd_params_t p, bd_stats_t* out) {
+template <int MINB>
+__global__ void __launch_bounds__(STEP_BT, MINB) k_step_abp_grid(bd_state_t s, bd_params_t p, bd_stats_t* out) {
     Ctx c = make_ctx(s, p);
     ExecGrid x{c.w.ctl};
     step_abp(x, c, out);
@@ -310,8 +327,8 @@ void init_device_info() {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        int m = occupancy((const void*)k_step_tri_grid, STEP_BT);
-        const void* coop[] = {(const void*)k_restore_delaunay_grid, (const void*)k_op_grid, (const void*)k_step_abp_grid, (const void*)k_step_verlet_grid,
+        int m = occupancy((const void*)k_step_tri_grid<2>, STEP_BT);
+        const void* coop[] = {(const void*)k_restore_delaunay_grid, (const void*)k_op_grid, (const void*)k_step_abp_grid<2>, (const void*)k_step_verlet_grid<2>,
                               (const void*)k_verlet_build_grid, (const void*)k_short_range_grid,
                               (const void*)k_overlap_pass_grid};
         for (const void* f : coop) {
@@ -319,6 +336,13 @@ void init_device_info() {
             m = o < m ? o : m;
         }
         g_grid_blocks_per_sm = m;
+        int mw = occupancy((const void*)k_step_tri_grid<WIDE_MINB>, STEP_BT);
+        const void* wide[] = {(const void*)k_step_verlet_grid<WIDE_MINB>, (const void*)k_step_abp_grid<WIDE_MINB>};
+        for (const void* f : wide) {
+            const int o = occupancy(f, STEP_BT);
+            mw = o < mw ? o : mw;
+        }
+        g_wide_blocks_per_sm = mw;
         g_lr_blocks_per_sm[1] = occupancy((const void*)k_allpairs<true>, LR_BT);
         g_lr_blocks_per_sm[0] = occupancy((const void*)k_allpairs<false>, LR_BT);
         g_fast_blocks_per_sm = occupancy((const void*)k_allpairs_fast, FS_BT);
@@ -326,9 +350,9 @@ void init_device_info() {
     });
 }
 
-int grid_blocks(int64_t work_items) {
+int grid_blocks(int64_t work_items, bool wide = false) {
     int64_t want = (work_items + STEP_BT - 1) / STEP_BT;
-    int64_t cap = (int64_t)g_num_sms * g_grid_blocks_per_sm;
+    int64_t cap = (int64_t)g_num_sms * (wide ? g_wide_blocks_per_sm : g_grid_blocks_per_sm);
     if (cap > 4096) cap = 4096;
     if (want > cap) want = cap;
     return (int)(want < 1 ? 1 : want);
@@ -342,8 +366,8 @@ unsigned grid_for(int64_t items, int bt = 256) {
     return (unsigned)(nb < 1 ? 1 : nb);
 }
 
-int coop_launch(const void* f, int64_t items, void** args, cudaStream_t st) {
-    return err_code(cudaLaunchCooperativeKernel(f, dim3(grid_blocks(items)), dim3(STEP_BT), args, 0, st));
+int coop_launch(const void* f, int64_t items, void** args, cudaStream_t st, bool wide = false) {
+    return err_code(cudaLaunchCooperativeKernel(f, dim3(grid_blocks(items, wide)), dim3(STEP_BT), args, 0, st));
 }
 
 // ---- all-pairs launches ------------------------------------------------------
@@ -452,8 +476,8 @@ int launch_force(const bd_state_t* s, const bd_params_t* p, cudaStream_t st) {
                      s->force_err, st);
 }
 
-int launch_driver(const void* grid_fn, const void* block_fn, const bd_state_t* s, const bd_params_t* p,
-                  bd_stats_t* out, cudaStream_t st) {
+int launch_driver(const void* grid_fn, const void* wide_fn, const void* block_fn, const bd_state_t* s,
+                  const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
     init_device_info();
     bd_state_t sv = *s;
     bd_params_t pv = *p;
@@ -462,11 +486,13 @@ int launch_driver(const void* grid_fn, const void* block_fn, const bd_state_t* s
         return err_code(cudaLaunchKernel(block_fn, dim3(1), dim3(BLOCK_BT), args, 0, st));
     int64_t items = s->tri.ne > p->n ? s->tri.ne : p->n;
     if (p->pair_capacity > items) items = p->pair_capacity;
+    if (p->n >= wide_min_n()) return coop_launch(wide_fn, items, args, st, true);
     return coop_launch(grid_fn, items, args, st);
 }
 
 int launch_maintain_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
-    return launch_driver((const void*)k_step_tri_grid, (const void*)k_step_tri_block, s, p, out, st);
+    return launch_driver((const void*)k_step_tri_grid<2>, (const void*)k_step_tri_grid<WIDE_MINB>,
+                         (const void*)k_step_tri_block, s, p, out, st);
 }
 
 int launch_step_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
@@ -476,7 +502,8 @@ int launch_step_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, 
 }
 
 int launch_step_verlet(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
-    return launch_driver((const void*)k_step_verlet_grid, (const void*)k_step_verlet_block, s, p, out, st);
+    return launch_driver((const void*)k_step_verlet_grid<2>, (const void*)k_step_verlet_grid<WIDE_MINB>,
+                         (const void*)k_step_verlet_block, s, p, out, st);
 }
 
 int launch_op(const bd_state_t* s, const bd_params_t* p, OpArgs a, int64_t items, cudaStream_t st) {
@@ -489,7 +516,8 @@ int launch_op(const bd_state_t* s, const bd_params_t* p, OpArgs a, int64_t items
 }
 
 int launch_step_abp(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
-    return launch_driver((const void*)k_step_abp_grid, (const void*)k_step_abp_block, s, p, out, st);
+    return launch_driver((const void*)k_step_abp_grid<2>, (const void*)k_step_abp_grid<WIDE_MINB>,
+                         (const void*)k_step_abp_block, s, p, out, st);
 }
 
 // a transient state for the standalone pair-list entry points

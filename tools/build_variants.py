@@ -9,9 +9,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1703_02484_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "sym_ct256_minb2": ["BD_SY_CT=256", "BD_SY_MINB=2"],
-    "sym_ct256_minb2_s32": ["BD_SY_CT=256", "BD_SY_MINB=2", "BD_SY_S=32"],
-    "sym_s32": ["BD_SY_S=32"],
 }
 
 if __name__ == "__main__":
