@@ -23,6 +23,15 @@ constexpr int STEP_BT = 256;
 // at 64 registers (4 CTAs per SM: twice the memory-level parallelism for the
 // dependent gathers of large N; 25 % faster at N = 1M, slower at 16k).
 constexpr int WIDE_MINB = 4;
+int64_t lrw_max_n() {  // BD_LRW_MAX_N overrides the EXACT warp-per-receiver threshold (tuning)
+    static int64_t v = -1;
+    if (v < 0) {
+        const char* e = getenv("BD_LRW_MAX_N");
+        v = e ? atoll(e) : LRW_MAX_N;
+    }
+    return v;
+}
+
 int64_t wide_min_n() {  // BD_WIDE_MIN_N overrides (tests: the two variants must agree bit for bit)
     static int64_t v = -1;
     if (v < 0) {
@@ -380,6 +389,11 @@ int launch_lr(const double4* src, const double* mu, int64_t n, const bd_params_t
     if (i1 <= i0) return 0;
     const int fast = precision == BD_LR_FAST;
     const int64_t R = i1 - i0;
+    if (!fast && n <= lrw_max_n()) {
+        k_allpairs_exact_warp<<<(unsigned)((R + LRW_WARPS - 1) / LRW_WARPS), LRW_WARPS * 32, 0, st>>>(
+            src, mu, n, p.L, p.mi_lo, p.mi_hi, i0, i1, out, err);
+        return err_code(cudaGetLastError());
+    }
     const int64_t nb_min = (R + LR_BT - 1) / LR_BT;
     const int64_t m = (nb_min + g_num_sms - 1) / g_num_sms;
     int64_t nb = m <= g_lr_blocks_per_sm[fast] ? (int64_t)g_num_sms * m : nb_min;
