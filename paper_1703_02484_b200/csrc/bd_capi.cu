@@ -359,9 +359,20 @@ void init_device_info() {
     });
 }
 
+int64_t grid_cap_per_sm() {  // BD_GRID_BLOCKS_PER_SM caps the persistent grids (tuning)
+    static int64_t v = -1;
+    if (v < 0) {
+        const char* e = getenv("BD_GRID_BLOCKS_PER_SM");
+        v = e ? atoll(e) : 0;
+    }
+    return v;
+}
+
 int grid_blocks(int64_t work_items, bool wide = false) {
     int64_t want = (work_items + STEP_BT - 1) / STEP_BT;
-    int64_t cap = (int64_t)g_num_sms * (wide ? g_wide_blocks_per_sm : g_grid_blocks_per_sm);
+    int64_t per = wide ? g_wide_blocks_per_sm : g_grid_blocks_per_sm;
+    if (grid_cap_per_sm() > 0 && grid_cap_per_sm() < per) per = grid_cap_per_sm();
+    int64_t cap = (int64_t)g_num_sms * per;
     if (cap > 4096) cap = 4096;
     if (want > cap) want = cap;
     return (int)(want < 1 ? 1 : want);
