@@ -73,9 +73,34 @@ BD_HD bool driver_enter(X& x, Red<X>& R, Ctx& c, bd_stats_t* out) {
 
 // LongRangeSimulation.step after the all-pairs force (dynamics.py:196-274).
 // s.force holds F_LR (force_mode LR / LRSR) from the all-pairs kernel.
+// phase timers for the breakdown in bd_stats_t.work (leader's clock, between barriers)
+template <class X>
+BD_HD int maintain_t(X& x, Red<X>& R, Ctx& c, int64_t* repairs, int64_t* flip_passes) {
+    const int64_t t0 = now_ns();
+    const int m = maintain(x, R, c, repairs, flip_passes);
+    c.work[WK_T_MAINTAIN] += now_ns() - t0;
+    return m;
+}
+
+template <class X, class PS>
+BD_HD int64_t correct_overlaps_t(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri) {
+    const int64_t t0 = now_ns();
+    const int64_t r = correct_overlaps(x, R, c, ps, tri);
+    c.work[WK_T_OVERLAP] += now_ns() - t0;
+    return r;
+}
+
+template <class X>
+BD_HD void build_edge_incidence_t(X& x, Ctx& c) {
+    const int64_t t0 = now_ns();
+    build_edge_incidence(x, c);
+    c.work[WK_T_INCIDENCE] += now_ns() - t0;
+}
+
 template <class X>
 BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
     Red<X> R(x);
+    const int64_t t_enter = now_ns();
     if (!driver_enter(x, R, c, out)) return;
     const int64_t rebuilds0 = c.s.vl_meta ? c.s.vl_meta[2] : 0;
     if (c.p.force_mode != BD_FORCE_SR && check_singular(x, R, c, c.s.force_err, out)) return;
@@ -108,7 +133,7 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
         if (nc) ph_apply_crossings(x, c);
         repairs = 0;
         flip_passes = 0;
-        int m = maintain(x, R, c, &repairs, &flip_passes);
+        int m = maintain_t(x, R, c, &repairs, &flip_passes);
         if (m < 0) break;
         failed = m == 1;
         if (!failed) {
@@ -116,12 +141,12 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
             for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) c.s.overlap_flags[i] = 0;
             int64_t outer;
             for (outer = 0; outer < c.p.max_overlap_iters; ++outer) {
-                build_edge_incidence(x, c);
-                const int64_t ri = correct_overlaps(x, R, c, EdgePairs{c.s.tri.edge_v, c.s.tri.ne}, true);
+                build_edge_incidence_t(x, c);
+                const int64_t ri = correct_overlaps_t(x, R, c, EdgePairs{c.s.tri.edge_v, c.s.tri.ne}, true);
                 if (ri < 0) break;
                 iters += ri;
                 if (ri == 0) break;
-                m = maintain(x, R, c, &repairs, &flip_passes);
+                m = maintain_t(x, R, c, &repairs, &flip_passes);
                 if (m < 0) break;
                 failed = m == 1;
                 if (failed) break;
@@ -163,6 +188,7 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
         out->status = (int64_t)c.w.ctl->status;
         out->err_i = (int64_t)c.w.ctl->err_i;
         out->err_k = (int64_t)c.w.ctl->err_k;
+        c.work[WK_T_TOTAL] = now_ns() - t_enter;
         for (int k = 0; k < WK_N; ++k) out->work[k] = c.work[k];
         *c.s.call = c.call;
     }

@@ -137,6 +137,10 @@ enum {
     WK_INCIDENCE,      // incidence-list builds
     WK_VL_REBUILD,     // Verlet list rebuilds
     WK_SR_FORCE,       // short-range force evaluations
+    WK_T_MAINTAIN,     // ns in pass-through check + inversion repair + Delaunay restoration
+    WK_T_OVERLAP,      // ns in overlap sweeps
+    WK_T_INCIDENCE,    // ns in incidence-list builds
+    WK_T_TOTAL,        // ns from driver entry to exit
     WK_N
 };
 
@@ -150,6 +154,17 @@ struct Ctx {
 
 BD_HD void ctx_init_work(Ctx& c) {
     for (int k = 0; k < WK_N; ++k) c.work[k] = 0;
+}
+
+// device wall clock (ns) for the phase breakdown; 0 on the host emulation
+BD_HD int64_t now_ns() {
+#if defined(__CUDA_ARCH__)
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return (int64_t)t;
+#else
+    return 0;
+#endif
 }
 
 template <class X>

@@ -37,6 +37,14 @@ def step_bytes(work: dict, n: int, ne: int, nt: int, pairs: int = 0, overlap_pai
     return int(sum(PASS_BYTES[k](n, ne, nt, pairs, q) * int(v) for k, v in work.items() if k in PASS_BYTES))
 
 
+def phase_breakdown(work: dict) -> dict:
+    """Share of the step kernel's time per phase group (device clock of the leader thread)."""
+    tot = max(int(work.get("t_total_ns", 0)), 1)
+    out = {k[2:-3]: work.get(k, 0) / tot for k in ("t_maintain_ns", "t_overlap_ns", "t_incidence_ns")}
+    out["other"] = max(0.0, 1.0 - sum(out.values()))
+    return out
+
+
 def hbm_peak_gbs(measured: dict, default: float = 6538.6) -> float:
     """HBM copy bandwidth from MEASURED_PEAKS.json (driver-written), else the recipe's figure."""
     for key in ("hbm_gbs", "hbm_copy_gbs", "hbm_burst_gbs", "hbm_GBps"):

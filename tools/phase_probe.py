@@ -32,6 +32,10 @@ for do_flush in (True, False):
     st = [_decode_stats(r) for r in stats[:10].cpu().numpy()]
     print(f"flush={do_flush}: force {np.mean(fm):.3f} ms, maintain {np.mean(mm):.3f} ms (min {np.min(mm):.3f}); "
           f"sweeps/step {np.mean([s['overlap_iterations'] for s in st]):.1f} flip passes {np.mean([s['flip_passes'] for s in st]):.1f}")
+    from paper_1703_02484_b200.roofline import phase_breakdown
+    w = {k: float(np.mean([s['work'][k] for s in st])) for k in st[0]['work']}
+    print("   work/step:", {k: round(v, 1) for k, v in w.items()})
+    print("   time shares:", {k: round(v, 3) for k, v in phase_breakdown(w).items()})
 # host-side launch cost of the driver
 t0 = time.perf_counter()
 for j in range(10):
