@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--n", type=int, default=131072)
     ap.add_argument("--rho", type=float, default=0.3)
     ap.add_argument("--precision", default="auto", choices=["auto", "fast-sym", "fast", "exact"],
-                    help="auto: fast-sym on one GPU (Newton's third law on r^-3), fast when sharded")
+                    help="auto = fast-sym (Newton's third law on r^-3; sharded by block pairs + all-reduce)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -195,7 +195,7 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
     n = args.n
     if args.precision == "auto":
-        args.precision = "fast-sym" if world == 1 else "fast"
+        args.precision = "fast-sym"
     box, pos, types, alpha, mu = workload(n, args.rho)
     t_setup = time.perf_counter()
     sys_ = ParticleSystem(pos, types, alpha, mu, box)
@@ -205,13 +205,18 @@ def run_ours(args):
     kw = {}
     if world > 1:
         from paper_1703_02484_b200.distributed import ShardedLongRange
-        gather = None
+        gather = reduce = None
         if gloo_test:
             def gather(buf, mine):
                 parts = [torch.empty_like(mine, device="cpu") for _ in range(world)]
                 dist.all_gather(parts, mine.cpu())
                 buf.copy_(torch.cat(parts, 0).to(buf.device))
-        kw["sharding"] = ShardedLongRange(rank, world, gather=gather)
+
+            def reduce(part):
+                h = part.cpu()
+                dist.all_reduce(h)
+                part.copy_(h.to(part.device))
+        kw["sharding"] = ShardedLongRange(rank, world, gather=gather, reduce=reduce)
     sim = LongRangeSimulation(sys_, params, CounterRng(0, 2), tri=tri, precision=args.precision, **kw)
     t_setup = time.perf_counter() - t_setup
     sim.run(args.warmup)
@@ -310,9 +315,10 @@ def run_ours(args):
                    "sample": f"failed: {exc}"}
     kname = {"fast-sym": "k_allpairs_sym", "fast": "k_allpairs_fast", "exact": "k_allpairs"}[args.precision]
     traffic, pipe = profiled_traffic(kname)
-    # kernels of ours per step: sort (4) + pack + pair kernel + combine/reduce + unsort + rescan, then the
-    # persistent step kernel (fast / fast-sym); pack + pair kernel + step kernel (exact); +2 slot copies sharded
-    launches_per_step = (10 if args.precision != "exact" else 3) + (0 if world == 1 or args.precision != "exact" else 2)
+    # kernels of ours per step: sort (4) + pack + pair kernel + partial sums + finish + unsort + rescan
+    # (fast-sym); sort (4) + pack + pair kernel + partition sums + unsort + rescan (fast); pack + pair
+    # kernel (+ slot copy in / out when sharded) (exact); then the persistent step kernel
+    launches_per_step = {"fast-sym": 11, "fast": 10, "exact": 3 if world == 1 else 5}[args.precision]
     line = {
         "metric": "particle-steps/s (N x steps / s), long-range all-pairs + Delaunay maintenance + overlap correction",
         "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": K, "warmup": args.warmup,

@@ -51,8 +51,9 @@ extern "C" {
 #define BD_LR_FAST 1
 /* FAST-SYM: FAST arithmetic with each unordered pair's r^-3 evaluated once
  * and applied to both directions (Newton's third law on the geometric
- * factor; csrc/bd_allpairs_sym.cuh).  Single GPU, whole range only;
- * workspace ~ n^2/32 bytes (bd_long_range_workspace_bytes_for). */
+ * factor; csrc/bd_allpairs_sym.cuh).  Whole range only (shard it with
+ * bd_force_sym_partial / _finish); workspace ~ n^2/64 bytes
+ * (bd_long_range_workspace_bytes_for). */
 #define BD_LR_FAST_SYM 2
 
 /* PeriodicTriangulation arrays, triangulation.py:129-139 */
@@ -197,6 +198,16 @@ int bd_force_prepare(const bd_state_t* s, const bd_params_t* p, void* stream);
 int bd_force_slots(const bd_state_t* s, const bd_params_t* p, int64_t s0, int64_t s1, double* slot3,
                    void* stream);
 int bd_force_finish(const bd_state_t* s, const bd_params_t* p, const double* slot3, void* stream);
+
+/* The FAST-SYM force (p->lr_precision == BD_LR_FAST_SYM) in two calls, for
+ * sharding: every rank runs _sym_partial for its share of the circulant
+ * block pairs (rank of world), writing the unscaled per-slot partial
+ * P_r = A_r - B_r into part (n,2); the ranks all-reduce (sum) part (NCCL);
+ * _sym_finish forms F = mu P and scatters it into s->force / s->force_err.
+ * Deterministic for a given world size. */
+int bd_force_sym_partial(const bd_state_t* s, const bd_params_t* p, int rank, int world, double* part,
+                         void* stream);
+int bd_force_sym_finish(const bd_state_t* s, const bd_params_t* p, const double* part, void* stream);
 
 /* the rest of LongRangeSimulation.step after the force (dynamics.py:196-274):
  * integrate, pass-through check, inversion repair, Delaunay restoration,

@@ -88,6 +88,8 @@ def _protos():
         "bd_force_prepare": ([P(BdState), P(BdParams), c_vp], c_int),
         "bd_force_slots": ([P(BdState), P(BdParams), c_i64, c_i64, c_vp, c_vp], c_int),
         "bd_force_finish": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
+        "bd_force_sym_partial": ([P(BdState), P(BdParams), c_int, c_int, c_vp, c_vp], c_int),
+        "bd_force_sym_finish": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
         "bd_maintain_tri": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
         "bd_step_tri": ([P(BdState), P(BdParams), c_vp], c_int),
         "bd_run_tri": ([P(BdState), P(BdParams), c_i64, c_vp, c_vp], c_int),
@@ -132,4 +134,4 @@ EXPORTS = ("bd_brute_overlaps", "bd_force","bd_force_prepare", "bd_force_slots",
            "bd_integrate", "bd_tri_apply_crossings", "bd_tri_edge_inversion", "bd_tri_signed_area2",
            "bd_tri_delaunay_flags", "bd_tri_inverted_edge_flags", "bd_tri_flip_edges", "bd_tri_repair_inversions",
            "bd_tri_restore_delaunay_ex", "bd_overlap_correct", "bd_tri_copy", "bd_step_abp", "bd_run_abp",
-           "bd_long_range_workspace_bytes_for")
+           "bd_long_range_workspace_bytes_for", "bd_force_sym_partial", "bd_force_sym_finish")

@@ -29,8 +29,11 @@
 //    per (d, source);
 //  * k_sym_combine sums the SY_S receiver partials and the D source
 //    partials of every slot in fixed order: F = mu (A - B).
-// Single-GPU only (the sharded path keeps the directed kernel, whose
-// per-receiver sums make results identical for every world size).
+// Multi-GPU: rank r of G owns the chunks [r S / G, (r+1) S / G) of every
+// block (and with them a contiguous range of distances d); it writes the
+// unscaled partial P_r = A_r - B_r of every slot, the ranks all-reduce P and
+// finish F = mu P.  Deterministic for a given G; the sum order (and so the
+// last bits) depends on G, unlike the directed FAST kernel.
 #pragma once
 
 #include "bd_allpairs_fast.cuh"
@@ -63,6 +66,14 @@ constexpr int SY_S = BD_SY_S;  // chunks of the circulant distance range (grid.y
 
 BD_HD int64_t sym_blocks(int64_t n) { return (n + SY_BT - 1) / SY_BT; }
 BD_HD int64_t sym_D(int64_t n) { return sym_blocks(n) / 2; }
+
+// chunk and distance ranges of rank r of G (see the header comment)
+struct SymRange {
+    int c0, c1;      // chunks [c0, c1)
+    int64_t d0, d1;  // source-side distances [d0, d1), d >= 1
+};
+
+BD_HD SymRange sym_range(int64_t n, int rank, int world);
 BD_HD int64_t sym_tiles(int64_t n) { return (n + SY_TS - 1) / SY_TS; }
 
 struct SymWs {
@@ -73,12 +84,13 @@ struct SymWs {
     double* apart;   // (SY_S, n, 2) receiver-side partial sums per chunk
     double* bpart;   // (D, n, 2) source-side partial sums per circulant distance
     double* slot3;   // (n, 3) fx, fy, flag per slot
+    double* part;    // (n, 2) P = A - B per slot (single GPU; ranks all-reduce their own)
 };
 
 BD_HD int64_t sym_ws_bytes(int64_t n) {
     const int64_t D = sym_D(n) > 0 ? sym_D(n) : 1;
     return fast_ws_bytes(n) + fs_align(32 * n) + fs_align(64 * n) + fs_align(32 * sym_tiles(n)) +
-           fs_align(16 * n * SY_S) + fs_align(16 * n * D) + fs_align(24 * n) + 256;
+           fs_align(16 * n * SY_S) + fs_align(16 * n * D) + fs_align(24 * n) + fs_align(16 * n) + 256;
 }
 
 BD_HD SymWs sym_ws_carve(void* base, int64_t n) {
@@ -91,7 +103,8 @@ BD_HD SymWs sym_ws_carve(void* base, int64_t n) {
     w.bbox = (uint64_t*)b; b += fs_align(32 * sym_tiles(n));
     w.apart = (double*)b; b += fs_align(16 * n * SY_S);
     w.bpart = (double*)b; b += fs_align(16 * n * D);
-    w.slot3 = (double*)b;
+    w.slot3 = (double*)b; b += fs_align(24 * n);
+    w.part = (double*)b;
     return w;
 }
 
@@ -335,7 +348,8 @@ constexpr int SY_NW2 = SY_CT / 32;   // warps per CTA
 constexpr int SY_SMEM = 2 * SY_TS * (int)sizeof(SrcS) + 2 * SY_NW2 * SY_TS * 16;
 
 // grid (Mb, SY_S), SY_CT threads; warp v of block I owns slots I*SY_BT + 64 v + {lane, lane + 32}
-__global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int64_t n, double L, double lo, double hi) {
+__global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int64_t n, double L, double lo, double hi,
+                                                                     int chunk0) {
     extern __shared__ __align__(128) unsigned char sy_smem[];
     SrcS* tiles = reinterpret_cast<SrcS*>(sy_smem);                              // [2][SY_TS]
     double* bw = reinterpret_cast<double*>(sy_smem + 2 * SY_TS * sizeof(SrcS));  // [2][SY_NW2][SY_TS][2]
@@ -343,7 +357,7 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t Mb = sym_blocks(n), D = sym_D(n);
     const int64_t I = blockIdx.x;
-    const int chunk = blockIdx.y;
+    const int chunk = chunk0 + (int)blockIdx.y;
 
     SymRecv r;
     int64_t slot[SY_R];
@@ -454,25 +468,33 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
     }
 }
 
-// F = mu (A - B) per slot, fixed summation order -> slot3 (fx, fy, flag)
-__global__ void k_sym_combine(int64_t n, SymWs w) {
+// P = A - B per slot over this rank's chunks / distances, fixed order -> part (n, 2)
+__global__ void k_sym_partial(int64_t n, SymWs w, SymRange g, double* __restrict__ part) {
     const int64_t Mb = sym_blocks(n), D = sym_D(n);
     const bool even = (Mb & 1) == 0;
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
-        for (int c = 0; c < SY_S; ++c) {
+        for (int c = g.c0; c < g.c1; ++c) {
             ax += w.apart[(size_t)c * n * 2 + 2 * s];
             ay += w.apart[(size_t)c * n * 2 + 2 * s + 1];
         }
         const int64_t J = s / SY_BT;
-        for (int64_t d = 1; d <= D; ++d) {
+        for (int64_t d = g.d0; d < g.d1; ++d) {
             const int64_t I = (J - d + Mb) % Mb;
             if (even && d == D && I >= Mb / 2) continue;  // that pair was done by block J as receiver
             bx += w.bpart[(size_t)(d - 1) * n * 2 + 2 * s];
             by += w.bpart[(size_t)(d - 1) * n * 2 + 2 * s + 1];
         }
+        part[2 * s] = ax - bx;
+        part[2 * s + 1] = ay - by;
+    }
+}
+
+// F = mu P per slot -> slot3 (fx, fy, flag)
+__global__ void k_sym_finish(int64_t n, SymWs w, const double* __restrict__ part) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         const double mu = w.src[s].mu;
-        const double fx = mu * (ax - bx), fy = mu * (ay - by);
+        const double fx = mu * part[2 * s], fy = mu * part[2 * s + 1];
         w.slot3[3 * s] = fx;
         w.slot3[3 * s + 1] = fy;
         w.slot3[3 * s + 2] = (isfinite(fx) && isfinite(fy)) ? 0.0 : -1.0;
@@ -480,5 +502,18 @@ __global__ void k_sym_combine(int64_t n, SymWs w) {
 }
 
 #endif  // __CUDACC__
+
+BD_HD SymRange sym_range(int64_t n, int rank, int world) {
+    SymRange g;
+    g.c0 = (int)((int64_t)rank * SY_S / world);
+    g.c1 = (int)((int64_t)(rank + 1) * SY_S / world);
+    const int64_t D = sym_D(n), per = (D + SY_S - 1) / SY_S;
+    const int64_t a = g.c0 == 0 ? 1 : 1 + (int64_t)g.c0 * per;  // chunk c >= 1 starts at 1 + c per
+    const int64_t b = 1 + (int64_t)g.c1 * per;
+    g.d0 = a < D + 1 ? a : D + 1;
+    g.d1 = b < D + 1 ? b : D + 1;
+    if (g.c1 <= g.c0) g.d1 = g.d0;
+    return g;
+}
 
 }  // namespace bd

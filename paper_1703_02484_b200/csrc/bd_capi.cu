@@ -460,9 +460,10 @@ int launch_fast_finish(const double* pos, int64_t n, const bd_params_t& p, const
     return err_code(cudaGetLastError());
 }
 
-// FAST-SYM (single GPU): sort, pack, symmetric pair kernel, combine, unsort
-int launch_sym(const double* pos, const double* alpha, const double* mu, int64_t n, const bd_params_t& p,
-               const SymWs& w, double* out, int64_t* err, cudaStream_t st) {
+// FAST-SYM stage 1 (every rank): sort + pack; pair kernel over this rank's
+// chunks; its partial P_r = A_r - B_r per slot into `part`
+int launch_sym_partial(const double* pos, const double* alpha, const double* mu, int64_t n, const bd_params_t& p,
+                       const SymWs& w, int rank, int world, double* part, cudaStream_t st) {
     init_device_info();
     if (n <= 0) return 0;
     const int64_t nc = fast_ncells(n);
@@ -473,11 +474,30 @@ int launch_sym(const double* pos, const double* alpha, const double* mu, int64_t
     k_sort_scatter<<<grid_for(n), 256, 0, st>>>(n, w.sort);
     k_sort_fix<<<grid_for(nc), 256, 0, st>>>(nc, w.sort);
     k_sym_pack<<<(unsigned)sym_tiles(n), SY_TS, 0, st>>>(pos, alpha, mu, n, p.L, p.mi_lo, p.mi_hi, w);
-    k_allpairs_sym<<<dim3((unsigned)sym_blocks(n), SY_S), SY_CT, SY_SMEM, st>>>(w, n, p.L, p.mi_lo, p.mi_hi);
-    k_sym_combine<<<grid_for(n), 256, 0, st>>>(n, w);
+    const SymRange g = sym_range(n, rank, world);
+    if (g.c1 > g.c0)
+        k_allpairs_sym<<<dim3((unsigned)sym_blocks(n), (unsigned)(g.c1 - g.c0)), SY_CT, SY_SMEM, st>>>(
+            w, n, p.L, p.mi_lo, p.mi_hi, g.c0);
+    k_sym_partial<<<grid_for(n), 256, 0, st>>>(n, w, g, part);
+    return err_code(cudaGetLastError());
+}
+
+// FAST-SYM stage 2: F = mu P (P summed over the ranks), unsort, exact re-scan of flagged receivers
+int launch_sym_finish(const double* pos, int64_t n, const bd_params_t& p, const SymWs& w, const double* part,
+                      double* out, int64_t* err, cudaStream_t st) {
+    if (n <= 0) return 0;
+    k_sym_finish<<<grid_for(n), 256, 0, st>>>(n, w, part);
     k_unsort_forces<<<grid_for(n), 256, 0, st>>>(0, n, w.sort, w.slot3, out, err);
     k_lr_rescan_pos<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, p.mi_lo, p.mi_hi, err);
     return err_code(cudaGetLastError());
+}
+
+// FAST-SYM on one GPU
+int launch_sym(const double* pos, const double* alpha, const double* mu, int64_t n, const bd_params_t& p,
+               const SymWs& w, double* out, int64_t* err, cudaStream_t st) {
+    int rc = launch_sym_partial(pos, alpha, mu, n, p, w, 0, 1, w.part, st);
+    if (rc) return rc;
+    return launch_sym_finish(pos, n, p, w, w.part, out, err, st);
 }
 
 int launch_force(const bd_state_t* s, const bd_params_t* p, cudaStream_t st) {
@@ -712,9 +732,25 @@ int bd_force(const bd_state_t* s, const bd_params_t* p, void* stream) {
 }
 
 // ---- sharded all-pairs force (multi-GPU: receiver slots per rank + all-gather)
+int bd_force_sym_partial(const bd_state_t* s, const bd_params_t* p, int rank, int world, double* part,
+                         void* stream) {
+    if (p->lr_precision != BD_LR_FAST_SYM || world < 1 || rank < 0 || rank >= world)
+        return -(int)cudaErrorInvalidValue;
+    const Ws w = ws_carve(s->work, *p, s->tri.ne, s->tri.nt);
+    return launch_sym_partial(s->pos, s->alpha, s->mu, p->n, *p, sym_ws_carve(w.src4, p->n), rank, world, part,
+                              (cudaStream_t)stream);
+}
+
+int bd_force_sym_finish(const bd_state_t* s, const bd_params_t* p, const double* part, void* stream) {
+    if (p->lr_precision != BD_LR_FAST_SYM) return -(int)cudaErrorInvalidValue;
+    const Ws w = ws_carve(s->work, *p, s->tri.ne, s->tri.nt);
+    return launch_sym_finish(s->pos, p->n, *p, sym_ws_carve(w.src4, p->n), part, s->force, s->force_err,
+                             (cudaStream_t)stream);
+}
+
 int bd_force_prepare(const bd_state_t* s, const bd_params_t* p, void* stream) {
     init_device_info();
-    if (p->lr_precision == BD_LR_FAST_SYM) return -(int)cudaErrorInvalidValue;  // single-GPU mode
+    if (p->lr_precision == BD_LR_FAST_SYM) return -(int)cudaErrorInvalidValue;  // bd_force_sym_partial
     cudaStream_t st = (cudaStream_t)stream;
     if (p->force_mode == BD_FORCE_SR) return 0;
     const Ws w = ws_carve(s->work, *p, s->tri.ne, s->tri.nt);

@@ -20,6 +20,7 @@ import ctypes
 import os
 from dataclasses import dataclass
 
+from ._abi import BD_LR_FAST_SYM
 from ._lib import check, lib
 
 
@@ -53,12 +54,14 @@ class ShardedLongRange:
     offset) into `buf`; by default torch.distributed.all_gather_into_tensor on
     the given group (NCCL on GPUs)."""
 
-    def __init__(self, rank: int, world: int, group=None, gather=None):
+    def __init__(self, rank: int, world: int, group=None, gather=None, reduce=None):
         self.rank = int(rank)
         self.world = int(world)
         self.group = group
         self._gather = gather
+        self._reduce = reduce
         self._buf = None
+        self._part = None
 
     @classmethod
     def from_env(cls, group=None):
@@ -81,8 +84,35 @@ class ShardedLongRange:
             self._buf = torch.zeros((rows, 3), dtype=torch.float64, device=device)
         return self._buf, sh
 
+    def reduce(self, part):
+        """Sum the per-rank FAST-SYM partials in place (all-reduce)."""
+        if self._reduce is not None:
+            return self._reduce(part)
+        import torch.distributed as dist
+        dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.group)
+
+    def part_buffer(self, n: int, device):
+        import torch
+        if self._part is None or self._part.shape[0] != n or self._part.device != device:
+            self._part = torch.zeros((n, 2), dtype=torch.float64, device=device)
+        return self._part
+
+    def force_sym(self, state, params, stream):
+        """FAST-SYM for a sharded group: this rank's share of the block pairs
+        -> per-slot partial, all-reduce (NCCL), finish."""
+        n = int(params.n)
+        part = self.part_buffer(n, self._device_of(state))
+        L = lib()
+        check(L.bd_force_sym_partial(ctypes.byref(state), ctypes.byref(params), self.rank, self.world,
+                                     ctypes.c_void_p(part.data_ptr()), stream), "bd_force_sym_partial")
+        self.reduce(part)
+        check(L.bd_force_sym_finish(ctypes.byref(state), ctypes.byref(params), ctypes.c_void_p(part.data_ptr()),
+                                    stream), "bd_force_sym_finish")
+
     def force(self, state, params, stream):
         """bd_force for a sharded group: prepare, own slots, all-gather, finish."""
+        if int(params.lr_precision) == BD_LR_FAST_SYM:
+            return self.force_sym(state, params, stream)
         n = int(params.n)
         buf, sh = self.buffer(n, self._device_of(state))
         s0, s1 = sh.bounds(n)
@@ -110,6 +140,20 @@ class SequentialShards(ShardedLongRange):
 
     def force(self, state, params, stream):
         n = int(params.n)
+        if int(params.lr_precision) == BD_LR_FAST_SYM:
+            # every rank's partial in turn, summed in rank order (the all-reduce)
+            import torch
+            L = lib()
+            dev = self._device_of(state)
+            total = torch.zeros((n, 2), dtype=torch.float64, device=dev)
+            part = torch.zeros((n, 2), dtype=torch.float64, device=dev)
+            for r in range(self.world):
+                check(L.bd_force_sym_partial(ctypes.byref(state), ctypes.byref(params), r, self.world,
+                                             ctypes.c_void_p(part.data_ptr()), stream), "bd_force_sym_partial")
+                total += part
+            check(L.bd_force_sym_finish(ctypes.byref(state), ctypes.byref(params), ctypes.c_void_p(total.data_ptr()),
+                                        stream), "bd_force_sym_finish")
+            return
         buf, _ = self.buffer(n, self._device_of(state))
         L = lib()
         check(L.bd_force_prepare(ctypes.byref(state), ctypes.byref(params), stream), "bd_force_prepare")

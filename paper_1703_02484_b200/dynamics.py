@@ -20,7 +20,8 @@ Extra keyword arguments of LongRangeSimulation (not in the reference):
                neighbour provider in every case;
   precision    "exact" (bit-identical to the reference), "fast-sym" (FAST
                arithmetic, each unordered pair's r^-3 evaluated once for both
-               directions; single GPU; workspace ~ n^2/32 bytes) or "fast" (sorted,
+               directions; sharded by block pairs + all-reduce; workspace
+               ~ n^2/64 bytes) or "fast" (sorted,
                FMA + rsqrt all-pairs; |dF|/|F| ~1e-13);
   skin         Verlet skin for the short-range force (default sigma / 2).
 """
@@ -362,8 +363,6 @@ class LongRangeSimulation(_SimulationBase):
             raise BrownsimError("short-range force requires params.r_cutoff")
         if precision not in PRECISIONS:
             raise BrownsimError(f"unknown precision {precision!r}; have {sorted(PRECISIONS)}")
-        if precision == "fast-sym" and sharding is not None and sharding.world > 1:
-            raise BrownsimError("precision 'fast-sym' is single-GPU; the sharded force uses 'fast' or 'exact'")
         self.force_model = force
         self.precision = precision
         self.skin = 0.5 * params.sigma if skin is None else float(skin)
