@@ -57,7 +57,7 @@ constexpr int SY_CT = BD_SY_CT;        // threads per CTA
 constexpr int SY_BT = SY_CT * SY_R;    // receivers per block
 constexpr int SY_TS = 256;  // sources per shared-memory stage
 #ifndef BD_SY_S
-#define BD_SY_S 32
+#define BD_SY_S 64
 #endif
 #ifndef BD_SY_MINB
 #define BD_SY_MINB 2

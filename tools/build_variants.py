@@ -9,8 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1703_02484_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "sym_minb3": ["BD_SY_MINB=3"],
-    "sym_ct128_minb6": ["BD_SY_CT=128", "BD_SY_MINB=6"],
+    "sym_s64": ["BD_SY_S=64"],
 }
 
 if __name__ == "__main__":

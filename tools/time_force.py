@@ -63,3 +63,32 @@ if os.environ.get("SLICES"):
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 3
         print(f"G={G}: per-rank slots force {ms:.3f} ms  (ideal {15.4 / G:.3f})")
+
+# per-rank share of the sharded FAST-SYM force: bd_force_sym_partial of rank 0 of G
+if os.environ.get("SYM_SLICES"):
+    import ctypes as C
+    from paper_1703_02484_b200 import _abi
+    from paper_1703_02484_b200.core import ParticleSystem, PeriodicBox, SimParams
+    from paper_1703_02484_b200.dynamics import make_params, _Engine
+    n = 131072
+    L = float(np.sqrt(n * np.pi * 0.25 / 0.3))
+    rng = np.random.default_rng(0)
+    pos = rng.uniform(0, L, size=(n, 2))
+    t = rng.integers(0, 2, n)
+    sys_ = ParticleSystem(pos, t, np.where(t == 0, 3.0, -3.0), np.where(t == 0, 3.0, -1.5), PeriodicBox(L))
+    bp = make_params(SimParams(n=n, sigma=1.0, dt=0.01, diffusion=0.01), L, 0, 2, 0, _abi.BD_LR_FAST_SYM)
+    eng = _Engine(sys_, None, bp, 0)
+    part = torch.zeros((n, 2), dtype=torch.float64, device="cuda")
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for G in (1, 2, 4, 8):
+        worst = 0.0
+        for r in range(G):
+            call = lambda: lib().bd_force_sym_partial(C.byref(eng.s), C.byref(bp), r, G, C.c_void_p(part.data_ptr()), st)
+            call(); torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(3):
+                call()
+            e1.record(); torch.cuda.synchronize()
+            worst = max(worst, e0.elapsed_time(e1) / 3)
+        print(f"G={G}: slowest rank's FAST-SYM partial {worst:.3f} ms")
