@@ -368,9 +368,10 @@ int64_t grid_cap_per_sm() {  // BD_GRID_BLOCKS_PER_SM caps the persistent grids 
     return v;
 }
 
-int grid_blocks(int64_t work_items, bool wide = false) {
+int grid_blocks(int64_t work_items, bool wide = false, int64_t per_sm_cap = 0) {
     int64_t want = (work_items + STEP_BT - 1) / STEP_BT;
     int64_t per = wide ? g_wide_blocks_per_sm : g_grid_blocks_per_sm;
+    if (per_sm_cap > 0 && per_sm_cap < per) per = per_sm_cap;
     if (grid_cap_per_sm() > 0 && grid_cap_per_sm() < per) per = grid_cap_per_sm();
     int64_t cap = (int64_t)g_num_sms * per;
     if (cap > 4096) cap = 4096;
@@ -386,8 +387,23 @@ unsigned grid_for(int64_t items, int bt = 256) {
     return (unsigned)(nb < 1 ? 1 : nb);
 }
 
-int coop_launch(const void* f, int64_t items, void** args, cudaStream_t st, bool wide = false) {
-    return err_code(cudaLaunchCooperativeKernel(f, dim3(grid_blocks(items, wide)), dim3(STEP_BT), args, 0, st));
+int coop_launch(const void* f, int64_t items, void** args, cudaStream_t st, bool wide = false,
+                int64_t per_sm_cap = 0) {
+    return err_code(
+        cudaLaunchCooperativeKernel(f, dim3(grid_blocks(items, wide, per_sm_cap)), dim3(STEP_BT), args, 0, st));
+}
+
+// Below this many particles the step drivers run one CTA per SM: the grid
+// barriers (~100 per step) dominate and get cheaper with fewer CTAs
+// (cfg2, N = 16k: 0.31 -> 0.25 ms per step); above it the phases' work
+// dominates and two CTAs per SM win (cfg3: 0.81 vs 1.0 ms).
+int64_t narrow_max_n() {  // BD_NARROW_MAX_N overrides (tests run both grid shapes on the goldens)
+    static int64_t v = -1;
+    if (v < 0) {
+        const char* e = getenv("BD_NARROW_MAX_N");
+        v = e ? atoll(e) : 65536;
+    }
+    return v;
 }
 
 // ---- all-pairs launches ------------------------------------------------------
@@ -532,7 +548,7 @@ int launch_driver(const void* grid_fn, const void* wide_fn, const void* block_fn
     int64_t items = s->tri.ne > p->n ? s->tri.ne : p->n;
     if (p->pair_capacity > items) items = p->pair_capacity;
     if (p->n >= wide_min_n()) return coop_launch(wide_fn, items, args, st, true);
-    return coop_launch(grid_fn, items, args, st);
+    return coop_launch(grid_fn, items, args, st, false, p->n < narrow_max_n() ? 1 : 0);
 }
 
 int launch_maintain_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
