@@ -254,7 +254,7 @@ def run_ours(args):
     host_stats = [_decode_stats(r) for r in stats_t.cpu().numpy()]
     bad = [st for st in host_stats if st["status"] != 0]
     # O(N) step (persistent maintenance kernel): algorithmic bytes from its work counters vs HBM
-    from paper_1703_02484_b200.roofline import hbm_peak_gbs, step_bytes
+    from paper_1703_02484_b200.roofline import hbm_peak_gbs, phase_roofline, step_bytes
     ne, nt = sim.tri.n_edges, sim.tri.n_triangles
     m_bytes = [step_bytes(st["work"], n, ne, nt) for st in host_stats]
     m_ms = [ev[j][1].elapsed_time(ev[j][2]) for j in range(K)]
@@ -351,6 +351,8 @@ def run_ours(args):
             "frac": float(np.sum(m_bytes) / (np.sum(m_ms) * 1e-3) / 1e9) / hbm_peak_gbs(measured_peaks()),
             "bytes_per_step": float(np.mean(m_bytes)),
             "work_per_step": {k: float(np.mean([st["work"][k] for st in host_stats])) for k in host_stats[0]["work"]},
+            "phases": phase_roofline({k: float(np.mean([st["work"][k] for st in host_stats]))
+                                      for k in host_stats[0]["work"]}, n, ne, nt),
             "note": "algorithmic bytes (SURVEY §8(d) per-pass minimum, paper_1703_02484_b200/roofline.py) of the "
                     "passes the kernel reports it ran, over its device time; the working set (~60 MB) is "
                     "L2-resident at this N and the kernel is grid-barrier/latency bound (profiles/)"},

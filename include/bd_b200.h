@@ -98,8 +98,10 @@ typedef struct bd_stats {
      * edge-inversion check, per-edge flag passes, per-triangle area passes,
      * independent-set rounds, flipped edges, overlap passes, overlap
      * gather/apply passes, incidence builds, Verlet rebuilds, short-range
-     * force evaluations, then 4 spare words */
-    int64_t work[16];
+     * force evaluations; then device time (ns) in maintenance, overlap
+     * sweeps, incidence builds, the whole driver, Verlet rebuilds and
+     * short-range forces; then spare words */
+    int64_t work[24];
 } bd_stats_t;
 
 /* device state of one simulation */

@@ -44,13 +44,13 @@ class BdStats(ctypes.Structure):
     _fields_ = [("dt_used", c_d), ("overlap_iterations", c_i64), ("flip_passes", c_i64),
                 ("inversion_repairs", c_i64), ("rollbacks", c_i64), ("n_overlapping", c_i64),
                 ("status", c_i64), ("err_i", c_i64), ("err_k", c_i64), ("rebuilds", c_i64),
-                ("reserved", c_i64 * 6), ("work", c_i64 * 16)]
+                ("reserved", c_i64 * 6), ("work", c_i64 * 24)]
 
 
 # bd_stats_t.work[] counters (csrc/bd_step.cuh WK_*)
 WORK_KEYS = ("integrate", "apply_crossings", "edge_inversion", "flag_pass", "area_pass", "lfmis_round", "flips",
              "overlap_pass", "overlap_apply", "incidence", "verlet_rebuild", "sr_force",
-             "t_maintain_ns", "t_overlap_ns", "t_incidence_ns", "t_total_ns")
+             "t_maintain_ns", "t_overlap_ns", "t_incidence_ns", "t_total_ns", "t_verlet_ns", "t_sr_force_ns")
 
 
 STATS_WORDS = ctypes.sizeof(BdStats) // 8

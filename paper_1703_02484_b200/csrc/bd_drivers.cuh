@@ -203,8 +203,10 @@ BD_HD int64_t overlap_rounds(X& x, Red<X>& R, Ctx& c, double margin) {
     int64_t iters = 0, round;
     for (round = 0; round < c.p.max_overlap_iters; ++round) {
         const SubsetPairs sp{c.s.pair_a, c.s.pair_b, c.w.ov_idx, (int64_t)x.ld((const u64*)&c.s.vl_meta[3])};
+        const int64_t t0 = now_ns();
         build_incidence(x, c.p.n, sp, c.w.inc_off, c.w.inc_cur, c.w.inc, c.work);
-        const int64_t ri = correct_overlaps(x, R, c, sp, false);
+        c.work[WK_T_INCIDENCE] += now_ns() - t0;
+        const int64_t ri = correct_overlaps_t(x, R, c, sp, false);
         if (ri < 0) break;
         iters += ri;
         if (!vl_stale(x, R, c)) break;
@@ -218,7 +220,8 @@ BD_HD int64_t overlap_rounds(X& x, Red<X>& R, Ctx& c, double margin) {
 }
 
 template <class X>
-BD_HD void verlet_stats(X& x, Red<X>& R, Ctx& c, bd_stats_t* out, int64_t rebuilds0, int64_t iters) {
+BD_HD void verlet_stats(X& x, Red<X>& R, Ctx& c, bd_stats_t* out, int64_t rebuilds0, int64_t iters,
+                        int64_t t_enter) {
     u64* r = R.open();
     for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) x.add(r, (u64)c.s.overlap_flags[i]);
     const u64 nov = R.close(r);
@@ -233,6 +236,7 @@ BD_HD void verlet_stats(X& x, Red<X>& R, Ctx& c, bd_stats_t* out, int64_t rebuil
         out->status = (int64_t)c.w.ctl->status;
         out->err_i = (int64_t)c.w.ctl->err_i;
         out->err_k = (int64_t)c.w.ctl->err_k;
+        c.work[WK_T_TOTAL] = now_ns() - t_enter;
         for (int k = 0; k < WK_N; ++k) out->work[k] = c.work[k];
         *c.s.call = c.call;
     }
@@ -244,6 +248,7 @@ BD_HD void verlet_stats(X& x, Red<X>& R, Ctx& c, bd_stats_t* out, int64_t rebuil
 template <class X>
 BD_HD void step_verlet(X& x, Ctx& c, bd_stats_t* out) {
     Red<X> R(x);
+    const int64_t t_enter = now_ns();
     if (!driver_enter(x, R, c, out)) return;
     const int64_t rebuilds0 = c.s.vl_meta[2];
     const double margin = c.p.sigma + c.p.skin;
@@ -258,7 +263,7 @@ BD_HD void step_verlet(X& x, Ctx& c, bd_stats_t* out) {
     c.call++;
     for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) c.s.overlap_flags[i] = 0;
     const int64_t iters = overlap_rounds(x, R, c, margin);
-    verlet_stats(x, R, c, out, rebuilds0, iters);
+    verlet_stats(x, R, c, out, rebuilds0, iters, t_enter);
 }
 
 // AbpSimulation.step move (dynamics.py:378-390): prev <- pos; pos =
@@ -301,6 +306,7 @@ BD_HD void ph_abp_move(X& x, Ctx& c) {
 template <class X>
 BD_HD void step_abp(X& x, Ctx& c, bd_stats_t* out) {
     Red<X> R(x);
+    const int64_t t_enter = now_ns();
     if (!driver_enter(x, R, c, out)) return;
     const int64_t rebuilds0 = c.s.vl_meta[2];
     const double margin = c.p.r_list;  // overlap_margin = r_list = sigma + skin (dynamics.py:366-367)
@@ -312,7 +318,7 @@ BD_HD void step_abp(X& x, Ctx& c, bd_stats_t* out) {
     c.call++;
     for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) c.s.overlap_flags[i] = 0;
     const int64_t iters = overlap_rounds(x, R, c, margin);
-    verlet_stats(x, R, c, out, rebuilds0, iters);
+    verlet_stats(x, R, c, out, rebuilds0, iters, t_enter);
 }
 
 }  // namespace bd

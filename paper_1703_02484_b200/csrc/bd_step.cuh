@@ -141,8 +141,12 @@ enum {
     WK_T_OVERLAP,      // ns in overlap sweeps
     WK_T_INCIDENCE,    // ns in incidence-list builds
     WK_T_TOTAL,        // ns from driver entry to exit
+    WK_T_VERLET,       // ns in Verlet list rebuilds (cell sort + ordered pair fill)
+    WK_T_SR_FORCE,     // ns in short-range force evaluations
     WK_N
 };
+
+static_assert(WK_N <= 24, "bd_stats_t.work has 24 words");
 
 struct Ctx {
     bd_params_t p;

@@ -107,7 +107,18 @@ BD_HD bool vl_stale(X& x, Red<X>& R, Ctx& c) {
 // when margin > 0, + the per-particle pair incidence for the force gather).
 // Returns false on a capacity overflow (status BD_ERR_CAPACITY).
 template <class X>
+BD_HD bool vl_rebuild_impl(X& x, Red<X>& R, Ctx& c, double margin);
+
+template <class X>
 BD_HD bool vl_rebuild(X& x, Red<X>& R, Ctx& c, double margin) {
+    const int64_t t0 = now_ns();
+    const bool ok = vl_rebuild_impl(x, R, c, margin);
+    c.work[WK_T_VERLET] += now_ns() - t0;
+    return ok;
+}
+
+template <class X>
+BD_HD bool vl_rebuild_impl(X& x, Red<X>& R, Ctx& c, double margin) {
     c.work[WK_VL_REBUILD]++;
     const int64_t n = c.p.n, ncx = c.p.ncx;
     int32_t* cnt = c.w.pcnt;
@@ -203,7 +214,17 @@ BD_HD bool vl_rebuild(X& x, Red<X>& R, Ctx& c, double margin) {
 
 // short_range_kernel (_kernels.py:62-91) gathered per particle: out[i], err[i]
 template <class X>
+BD_HD void sr_forces_impl(X& x, Ctx& c, double* out, int64_t* err);
+
+template <class X>
 BD_HD void sr_forces(X& x, Ctx& c, double* out, int64_t* err) {
+    const int64_t t0 = now_ns();
+    sr_forces_impl(x, c, out, err);
+    c.work[WK_T_SR_FORCE] += now_ns() - t0;
+}
+
+template <class X>
+BD_HD void sr_forces_impl(X& x, Ctx& c, double* out, int64_t* err) {
     c.work[WK_SR_FORCE]++;
     const double rc2 = c.p.r_cut * c.p.r_cut;
     const double* pos = c.s.pos;

@@ -37,20 +37,30 @@ def step_bytes(work: dict, n: int, ne: int, nt: int, pairs: int = 0, overlap_pai
     return int(sum(PASS_BYTES[k](n, ne, nt, pairs, q) * int(v) for k, v in work.items() if k in PASS_BYTES))
 
 
+PHASES = {  # pass kinds timed together (bd_stats_t.work timers)
+    "maintenance": (("edge_inversion", "flag_pass", "area_pass", "lfmis_round", "flips"), "t_maintain_ns"),
+    "overlap": (("overlap_pass", "overlap_apply", "apply_crossings"), "t_overlap_ns"),
+    "incidence": (("incidence",), "t_incidence_ns"),
+    "verlet": (("verlet_rebuild",), "t_verlet_ns"),
+    "sr_force": (("sr_force",), "t_sr_force_ns"),
+}
+
+
 def phase_breakdown(work: dict) -> dict:
     """Share of the step kernel's time per phase group (device clock of the leader thread)."""
     tot = max(int(work.get("t_total_ns", 0)), 1)
-    out = {k[2:-3]: work.get(k, 0) / tot for k in ("t_maintain_ns", "t_overlap_ns", "t_incidence_ns")}
+    out = {name: work.get(t, 0) / tot for name, (_, t) in PHASES.items()}
     out["other"] = max(0.0, 1.0 - sum(out.values()))
     return out
 
 
-def hbm_peak_gbs(measured: dict, default: float = 6538.6) -> float:
-    """HBM copy bandwidth from MEASURED_PEAKS.json (driver-written), else the recipe's figure."""
-    for key in ("hbm_gbs", "hbm_copy_gbs", "hbm_burst_gbs", "hbm_GBps"):
-        if key in measured:
-            try:
-                return float(measured[key])
-            except (TypeError, ValueError):
-                pass
-    return default
+def phase_roofline(work: dict, n: int, ne: int, nt: int, pairs: int = 0, overlap_pairs: int | None = None) -> dict:
+    """Achieved algorithmic bandwidth per phase group: {name: (bytes, ns, GB/s)}."""
+    q = ne if overlap_pairs is None else overlap_pairs
+    out = {}
+    for name, (kinds, t) in PHASES.items():
+        b = sum(PASS_BYTES[k](n, ne, nt, pairs, q) * work.get(k, 0) for k in kinds)
+        ns = work.get(t, 0)
+        if ns > 0:
+            out[name] = {"bytes": float(b), "ns": float(ns), "GBs": float(b / ns)}
+    return out

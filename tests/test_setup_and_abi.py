@@ -84,7 +84,7 @@ def test_struct_layouts_match_header(cuda_lib):
     """ctypes mirrors agree with the compiled layout (sizes via the workspace helpers)."""
     from paper_1703_02484_b200 import _abi
     assert ctypes.sizeof(_abi.BdTri) == 3 * 8 + 6 * 8
-    assert ctypes.sizeof(_abi.BdStats) == 32 * 8
+    assert ctypes.sizeof(_abi.BdStats) == 40 * 8
     p = _abi.BdParams()
     p.L, p.sigma, p.skin, p.r_cut = 100.0, 1.0, 0.5, 2.5
     cuda_lib.bd_prepare_params.argtypes = [ctypes.POINTER(_abi.BdParams)]

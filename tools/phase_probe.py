@@ -36,6 +36,8 @@ for do_flush in (True, False):
     w = {k: float(np.mean([s['work'][k] for s in st])) for k in st[0]['work']}
     print("   work/step:", {k: round(v, 1) for k, v in w.items()})
     print("   time shares:", {k: round(v, 3) for k, v in phase_breakdown(w).items()})
+    from paper_1703_02484_b200.roofline import phase_roofline
+    print("   phase GB/s:", {k: round(v["GBs"]) for k, v in phase_roofline(w, n, sim.tri.n_edges, sim.tri.n_triangles).items()})
 # host-side launch cost of the driver
 t0 = time.perf_counter()
 for j in range(10):

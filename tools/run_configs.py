@@ -105,8 +105,8 @@ def run(cfg_id, args):
     u0 = sim.sys.unwrapped_positions().clone()
     msd_t = sorted({int(round(v)) for v in np.logspace(0, np.log10(K), 25)} | {K})
     msd = []
-    from paper_1703_02484_b200.roofline import hbm_peak_gbs, step_bytes
-    dev_ms, maint_ms, mbytes, bad, checks, work_tot = 0.0, 0.0, 0, [], 0, {}
+    from paper_1703_02484_b200.roofline import hbm_peak_gbs, phase_roofline, step_bytes
+    dev_ms, maint_ms, mbytes, bad, checks, work_tot, pairs = 0.0, 0.0, 0, [], 0, {}, 0
     ne, nt = sim.tri.n_edges, sim.tri.n_triangles
     stats_tot = dict(overlap_iterations=0, flip_passes=0, inversion_repairs=0, rollbacks=0)
     done = 0
@@ -152,6 +152,7 @@ def run(cfg_id, args):
             "stats_total": stats_tot, "build_s": t_build, "cpu_baseline": cpu,
             "phase_ms": {"force": (dev_ms - maint_ms) / K, "maintain": maint_ms / K},
             "work_per_step": {k: v / K for k, v in work_tot.items()},
+            "phases": phase_roofline({k: v / K for k, v in work_tot.items()}, n, ne, nt, pairs),
             "maintain_roofline": {"bound": "hbm", "achieved": mbytes / (maint_ms * 1e-3) / 1e9, "unit": "GB/s",
                                   "peak": hbm_peak_gbs({}), "frac": mbytes / (maint_ms * 1e-3) / 1e9 / hbm_peak_gbs({}),
                                   "bytes_per_step": mbytes / K},
