@@ -21,7 +21,8 @@ Extra keyword arguments of LongRangeSimulation (not in the reference):
   precision    "exact" (bit-identical to the reference), "fast-sym" (FAST
                arithmetic, each unordered pair's r^-3 evaluated once for both
                directions; sharded by block pairs + all-reduce; workspace
-               ~ n^2/64 bytes) or "fast" (sorted,
+               ~ n^2/64 bytes), "auto" (fast-sym while that stays under
+               4 GiB, else fast) or "fast" (sorted,
                FMA + rsqrt all-pairs; |dF|/|F| ~1e-13);
   skin         Verlet skin for the short-range force (default sigma / 2).
 """
@@ -44,6 +45,7 @@ RESOLVE_FRAC = 1.0 - 1e-9  # dynamics.py:39
 
 FORCE_MODES = {"long-range": _abi.BD_FORCE_LR, "short-range": _abi.BD_FORCE_SR, "long+short": _abi.BD_FORCE_LRSR}
 PRECISIONS = {"exact": _abi.BD_LR_EXACT, "fast": _abi.BD_LR_FAST, "fast-sym": _abi.BD_LR_FAST_SYM}
+AUTO_SYM_MAX_BYTES = 4 << 30  # precision="auto": FAST-SYM up to ~500k particles (n^2/64 B of partials)
 
 
 @dataclass
@@ -361,8 +363,11 @@ class LongRangeSimulation(_SimulationBase):
             raise BrownsimError(f"unknown force model {force!r}; have {sorted(FORCE_MODES)}")
         if force != "long-range" and params.r_cutoff is None:
             raise BrownsimError("short-range force requires params.r_cutoff")
+        if precision == "auto":  # FAST-SYM while its partial buffer stays modest, else FAST
+            precision = "fast-sym" if lib().bd_long_range_workspace_bytes_for(sys.n, _abi.BD_LR_FAST_SYM) \
+                <= AUTO_SYM_MAX_BYTES else "fast"
         if precision not in PRECISIONS:
-            raise BrownsimError(f"unknown precision {precision!r}; have {sorted(PRECISIONS)}")
+            raise BrownsimError(f"unknown precision {precision!r}; have {sorted(PRECISIONS) + ['auto']}")
         self.force_model = force
         self.precision = precision
         self.skin = 0.5 * params.sigma if skin is None else float(skin)
