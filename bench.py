@@ -33,6 +33,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_1703_02484_b200.roofline import hbm_peak_gbs, phase_roofline, step_bytes  # noqa: E402
+
 C0 = [(0.5, 3.0, 3.0), (0.5, -3.0, -1.5)]
 FLOPS_PER_PAIR = 23  # algorithmic FP64 flops per directed pair (_kernels.py:48-56)
 
@@ -254,7 +256,6 @@ def run_ours(args):
     host_stats = [_decode_stats(r) for r in stats_t.cpu().numpy()]
     bad = [st for st in host_stats if st["status"] != 0]
     # O(N) step (persistent maintenance kernel): algorithmic bytes from its work counters vs HBM
-    from paper_1703_02484_b200.roofline import hbm_peak_gbs, phase_roofline, step_bytes
     ne, nt = sim.tri.n_edges, sim.tri.n_triangles
     m_bytes = [step_bytes(st["work"], n, ne, nt) for st in host_stats]
     m_ms = [ev[j][1].elapsed_time(ev[j][2]) for j in range(K)]

@@ -37,6 +37,17 @@ def step_bytes(work: dict, n: int, ne: int, nt: int, pairs: int = 0, overlap_pai
     return int(sum(PASS_BYTES[k](n, ne, nt, pairs, q) * int(v) for k, v in work.items() if k in PASS_BYTES))
 
 
+def hbm_peak_gbs(measured: dict, default: float = 6538.6) -> float:
+    """HBM copy bandwidth from MEASURED_PEAKS.json (driver-written), else the recipe's figure."""
+    for key in ("hbm_gbs", "hbm_copy_gbs", "hbm_burst_gbs", "hbm_GBps"):
+        if key in measured:
+            try:
+                return float(measured[key])
+            except (TypeError, ValueError):
+                pass
+    return default
+
+
 PHASES = {  # pass kinds timed together (bd_stats_t.work timers)
     "maintenance": (("edge_inversion", "flag_pass", "area_pass", "lfmis_round", "flips"), "t_maintain_ns"),
     "overlap": (("overlap_pass", "overlap_apply", "apply_crossings"), "t_overlap_ns"),

@@ -91,3 +91,24 @@ def test_struct_layouts_match_header(cuda_lib):
     cuda_lib.bd_prepare_params(ctypes.byref(p))
     assert p.r_list == 3.0 and p.ncx == 33
     assert p.mi_hi <= 50.0 and p.mi_lo >= -50.0
+
+
+def test_roofline_accounting_and_bench_imports():
+    """The host-side byte accounting used by bench.py / run_configs.py, and
+    that the measurement scripts import and parse their arguments on CPU."""
+    import subprocess
+    import sys
+    from paper_1703_02484_b200 import _abi
+    from paper_1703_02484_b200.roofline import hbm_peak_gbs, phase_breakdown, phase_roofline, step_bytes
+    work = {k: 0 for k in _abi.WORK_KEYS}
+    work.update(integrate=1, flag_pass=2, overlap_pass=3, t_maintain_ns=1000, t_overlap_ns=500, t_total_ns=2000)
+    n, ne, nt = 1000, 3000, 2000
+    assert step_bytes(work, n, ne, nt) == 64 * n + 2 * (11 * ne + 18 * nt + 16 * n) + 3 * (8 * ne + 32 * n)
+    ph = phase_roofline(work, n, ne, nt)
+    assert set(ph) == {"maintenance", "overlap"} and ph["overlap"]["GBs"] == 3 * (8 * ne + 32 * n) / 500
+    assert abs(sum(phase_breakdown(work).values()) - 1.0) < 1e-12
+    assert hbm_peak_gbs({"hbm_gbs": 6545.9}) == 6545.9 and hbm_peak_gbs({}) > 0
+    for script in ("bench.py", "tools/run_configs.py"):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, script), "--help"], capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]

@@ -31,6 +31,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+from paper_1703_02484_b200.roofline import hbm_peak_gbs, phase_roofline, step_bytes  # noqa: E402
+
 C0 = [(0.5, 3.0, 3.0), (0.5, -3.0, -1.5)]
 CFGS = {
     1: dict(n=1024, rho=0.3, force="long-range", precision="exact", steps=100, seed=0),
@@ -105,7 +107,6 @@ def run(cfg_id, args):
     u0 = sim.sys.unwrapped_positions().clone()
     msd_t = sorted({int(round(v)) for v in np.logspace(0, np.log10(K), 25)} | {K})
     msd = []
-    from paper_1703_02484_b200.roofline import hbm_peak_gbs, phase_roofline, step_bytes
     dev_ms, maint_ms, mbytes, bad, checks, work_tot, pairs = 0.0, 0.0, 0, [], 0, {}, 0
     ne, nt = sim.tri.n_edges, sim.tri.n_triangles
     stats_tot = dict(overlap_iterations=0, flip_passes=0, inversion_repairs=0, rollbacks=0)
