@@ -37,7 +37,7 @@ struct Ws {
     int32_t* cell_start; // (ncells+1)
     int32_t* cell_cur;   // (ncells)
     int32_t* corder;     // (n) stable cell order
-    int32_t* pcnt;       // (max(ncells, n)+1) pairs per cell (or per row) -> offsets
+    int32_t* pcnt;       // (max(5 n, ncells)+1) pairs per (cell, segment, particle) item (or per row) -> offsets
     int32_t* vinc_off;   // (n+1) CSR of Verlet pairs per particle
     int32_t* vinc_cur;   // (n)
     int32_t* vinc;       // (2 P)
@@ -81,7 +81,7 @@ BD_HD WsLayout ws_layout(const bd_params_t& p, int64_t ne, int64_t nt) {
     l.cell_start = o; o = align_up(o + (P ? 4 * (nc + 1) : 0));
     l.cell_cur = o; o = align_up(o + (P ? 4 * nc : 0));
     l.corder = o; o = align_up(o + (P ? 4 * n : 0));
-    l.pcnt = o; o = align_up(o + (P ? 4 * ((nc > n ? nc : n) + 1) : 0));
+    l.pcnt = o; o = align_up(o + (P ? 4 * ((nc > 5 * n ? nc : 5 * n) + 1) : 0));
     l.vinc_off = o; o = align_up(o + (P ? 4 * (n + 1) : 0));
     l.vinc_cur = o; o = align_up(o + (P ? 4 * n : 0));
     l.vinc = o; o = align_up(o + 8 * P);

@@ -23,46 +23,52 @@ namespace bd {
 BD_HD int off_x(int k) { return k == 0 ? 1 : (k == 1 ? -1 : (k == 2 ? 0 : 1)); }
 BD_HD int off_y(int k) { return k == 0 ? 0 : 1; }
 
-// pairs of one cell in the reference's nested-loop order; FILL writes them
+// The reference emits the pairs of cell c (ascending c) in the order
+//   segment 0: same cell, ia < ib;  segments 1..4: neighbour offsets
+//   (1,0), (-1,1), (0,1), (1,1), a in c x b in d   (_kernels.py:141-236),
+// a ascending inside every segment.  One work item per (cell, segment, a):
+// its pairs are contiguous in that order, so items are counted, scanned in
+// (cell, segment, a) order and filled independently -- 5 N short items
+// instead of one long sequential walk per cell.  Item index of sorted slot
+// s (particle corder[s] in cell c, local index s - start_c) and segment g:
+//   5 start_c + g m_c + (s - start_c),   m_c = particles in c.
+BD_HD int64_t vl_item(const Ctx& c, int64_t s, int g, int64_t* cell, int64_t* ia) {
+    const int64_t a = c.w.corder[s];
+    const int64_t cc = c.w.cell_id[a];
+    const int64_t st = c.w.cell_start[cc], m = c.w.cell_start[cc + 1] - st;
+    *cell = cc;
+    *ia = s - st;
+    return 5 * st + (int64_t)g * m + (s - st);
+}
+
 template <bool FILL>
-BD_HD int64_t cell_pairs_of(const Ctx& c, int64_t cell, int64_t k0) {
+BD_HD int64_t item_pairs_of(const Ctx& c, int64_t cell, int64_t ia, int g, int64_t k0) {
     const int64_t ncx = c.p.ncx;
     const int64_t cx = cell % ncx, cy = cell / ncx;
-    const int32_t a0 = c.w.cell_start[cell], a1 = c.w.cell_start[cell + 1];
+    const int32_t a0 = c.w.cell_start[cell];
     const double rl2 = c.p.r_list * c.p.r_list;
     const double* pos = c.s.pos;
-    int64_t k = k0;
-    for (int32_t ia = a0; ia < a1; ++ia) {
-        const int64_t a = c.w.corder[ia];
-        for (int32_t ib = ia + 1; ib < a1; ++ib) {
-            const int64_t b = c.w.corder[ib];
-            const double dx = mi_exact(pos[2 * a] - pos[2 * b], c.p), dy = mi_exact(pos[2 * a + 1] - pos[2 * b + 1], c.p);
-            if (dx * dx + dy * dy <= rl2) {
-                if (FILL) {
-                    c.s.pair_a[k] = a;
-                    c.s.pair_b[k] = b;
-                }
-                ++k;
-            }
-        }
+    const int64_t a = c.w.corder[a0 + ia];
+    const double xa = pos[2 * a], ya = pos[2 * a + 1];
+    int32_t b0, b1;
+    if (g == 0) {
+        b0 = a0 + (int32_t)ia + 1;
+        b1 = c.w.cell_start[cell + 1];
+    } else {
+        const int64_t d = ((cx + off_x(g - 1) + ncx) % ncx) + ((cy + off_y(g - 1)) % ncx) * ncx;
+        b0 = c.w.cell_start[d];
+        b1 = c.w.cell_start[d + 1];
     }
-    for (int off = 0; off < 4; ++off) {
-        const int64_t d = ((cx + off_x(off) + ncx) % ncx) + ((cy + off_y(off)) % ncx) * ncx;
-        const int32_t b0 = c.w.cell_start[d], b1 = c.w.cell_start[d + 1];
-        for (int32_t ia = a0; ia < a1; ++ia) {
-            const int64_t a = c.w.corder[ia];
-            for (int32_t ib = b0; ib < b1; ++ib) {
-                const int64_t b = c.w.corder[ib];
-                const double dx = mi_exact(pos[2 * a] - pos[2 * b], c.p),
-                             dy = mi_exact(pos[2 * a + 1] - pos[2 * b + 1], c.p);
-                if (dx * dx + dy * dy <= rl2) {
-                    if (FILL) {
-                        c.s.pair_a[k] = a;
-                        c.s.pair_b[k] = b;
-                    }
-                    ++k;
-                }
+    int64_t k = k0;
+    for (int32_t ib = b0; ib < b1; ++ib) {
+        const int64_t b = c.w.corder[ib];
+        const double dx = mi_exact(xa - pos[2 * b], c.p), dy = mi_exact(ya - pos[2 * b + 1], c.p);
+        if (dx * dx + dy * dy <= rl2) {
+            if (FILL) {
+                c.s.pair_a[k] = a;
+                c.s.pair_b[k] = b;
             }
+            ++k;
         }
     }
     return k - k0;
@@ -161,8 +167,14 @@ BD_HD bool vl_rebuild_impl(X& x, Red<X>& R, Ctx& c, double margin) {
             }
         }
         x.sync();
-        for (int64_t k = x.tid(); k < nc; k += x.nth()) cnt[k] = (int32_t)cell_pairs_of<false>(c, k, 0);
-        rows = nc;
+        for (int64_t t = x.tid(); t < 5 * n; t += x.nth()) {
+            const int64_t sl = t / 5;
+            const int g = (int)(t % 5);
+            int64_t cell, ia;
+            const int64_t item = vl_item(c, sl, g, &cell, &ia);
+            cnt[item] = (int32_t)item_pairs_of<false>(c, cell, ia, g, 0);
+        }
+        rows = 5 * n;
     } else {
         for (int64_t a = x.tid(); a < n; a += x.nth()) cnt[a] = (int32_t)brute_pairs_of<false>(c, a, 0);
         rows = n;
@@ -176,7 +188,13 @@ BD_HD bool vl_rebuild_impl(X& x, Red<X>& R, Ctx& c, double margin) {
         return false;
     }
     if (ncx >= 3)
-        for (int64_t k = x.tid(); k < rows; k += x.nth()) cell_pairs_of<true>(c, k, cnt[k]);
+        for (int64_t t = x.tid(); t < 5 * n; t += x.nth()) {
+            const int64_t sl = t / 5;
+            const int g = (int)(t % 5);
+            int64_t cell, ia;
+            const int64_t item = vl_item(c, sl, g, &cell, &ia);
+            item_pairs_of<true>(c, cell, ia, g, cnt[item]);
+        }
     else
         for (int64_t a = x.tid(); a < rows; a += x.nth()) brute_pairs_of<true>(c, a, cnt[a]);
     for (int64_t i = x.tid(); i < 2 * n; i += x.nth()) c.s.vl_snap[i] = c.s.pos[i];
