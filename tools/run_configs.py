@@ -100,7 +100,7 @@ def run(cfg_id, args):
         cfg["steps"] = args.steps
     sim, init, t_build = build(cfg)
     n, K = cfg["n"], cfg["steps"]
-    every = args.check_every or {1: 1, 2: 1, 4: 5, 5: 100}[cfg_id]
+    every = args.check_every or {1: 1, 2: 1, 4: 1, 5: 10}[cfg_id]
     brute = n <= 131072
     sim.run(3)  # warm-up (JIT-free, but first-touch / caches)
     torch.cuda.synchronize()
