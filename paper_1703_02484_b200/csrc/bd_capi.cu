@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(STEP_BT) k_overlap_pass_grid(bd_state_t s, bd_
             c.w.contrib[2 * e + 1] = delta * (dy / rr);
         }
         c.w.eovl[e] = (uint8_t)ov;
-        x.add(r, (u64)ov);
+        R.add((u64)ov);
     }
     const u64 cnt = R.close(r);
     for (int64_t i = x.tid(); i < p.n; i += x.nth()) {

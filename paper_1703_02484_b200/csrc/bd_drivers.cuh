@@ -21,7 +21,7 @@ BD_HD bool check_singular(X& x, Red<X>& R, Ctx& c, const int64_t* err, bd_stats_
     for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
         const bool bad = err[i] != 0;
         if (bad) x.umin(&c.w.ctl->scratch[1], (u64)i);
-        x.add(r, (u64)bad);
+        R.add((u64)bad);
     }
     if (!R.close(r)) return false;
     if (x.leader()) {
@@ -46,7 +46,7 @@ BD_HD bool check_finite(X& x, Red<X>& R, Ctx& c, bd_stats_t* out) {
     for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
         const bool bad = !(isfinite(c.s.force[2 * i]) && isfinite(c.s.force[2 * i + 1]));
         if (bad) x.umin(&c.w.ctl->scratch[0], (u64)i);
-        x.add(r, (u64)bad);
+        R.add((u64)bad);
     }
     if (!R.close(r)) return false;
     if (x.leader()) {
@@ -104,33 +104,45 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
     if (!driver_enter(x, R, c, out)) return;
     const int64_t rebuilds0 = c.s.vl_meta ? c.s.vl_meta[2] : 0;
     if (c.p.force_mode != BD_FORCE_SR && check_singular(x, R, c, c.s.force_err, out)) return;
+    int64_t tp = now_ns();
     if (c.p.force_mode != BD_FORCE_LR) {
         // short-range force over a Verlet list kept fresh by the rebuild rule
-        if (vl_stale(x, R, c) && !vl_rebuild(x, R, c, 0.0)) {
+        const bool stale = vl_stale(x, R, c);
+        c.work[WK_PROBE0] = now_ns() - tp;
+        if (stale && !vl_rebuild(x, R, c, 0.0)) {
             if (x.leader()) out->status = BD_ERR_CAPACITY;
             return;
         }
         sr_forces(x, c, c.w.sr_force, c.w.sr_err);
+        tp = now_ns();
         if (check_singular(x, R, c, c.w.sr_err, out)) return;
         const bool add = c.p.force_mode == BD_FORCE_LRSR;
         for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth())
             c.s.force[i] = add ? c.s.force[i] + c.w.sr_force[i] : c.w.sr_force[i];
         x.sync();
+        c.work[WK_PROBE1] = now_ns() - tp;
     }
+    tp = now_ns();
     if (check_finite(x, R, c, out)) return;
+    c.work[WK_PROBE2] = now_ns() - tp;
+    tp = now_ns();
     // save_state (triangulation.py:158-160) + image counters
     ph_tri_copy(x, c.s.tri, c.s.tri_backup);
     if (c.s.image)
         for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.w.image_bk[i] = c.s.image[i];
     x.sync();
+    c.work[WK_PROBE3] = now_ns() - tp;
 
     double dt_try = c.p.dt;
     int64_t rollbacks = 0, iters = 0, repairs = 0, flip_passes = 0;
     bool failed = false;
+    c.work[WK_T_PRE] = now_ns() - t_enter;
     for (;;) {
+        const int64_t t_int = now_ns();
         const u64 nc = ph_integrate(x, R, c, dt_try);
         c.call++;
         if (nc) ph_apply_crossings(x, c);
+        c.work[WK_T_INTEGRATE] += now_ns() - t_int;
         repairs = 0;
         flip_passes = 0;
         int m = maintain_t(x, R, c, &repairs, &flip_passes);
@@ -175,7 +187,7 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
     }
     // n_overlapping
     u64* r = R.open();
-    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) x.add(r, (u64)c.s.overlap_flags[i]);
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) R.add((u64)c.s.overlap_flags[i]);
     const u64 nov = R.close(r);
     if (x.leader()) {
         out->rebuilds = c.s.vl_meta ? c.s.vl_meta[2] - rebuilds0 : 0;
@@ -223,7 +235,7 @@ template <class X>
 BD_HD void verlet_stats(X& x, Red<X>& R, Ctx& c, bd_stats_t* out, int64_t rebuilds0, int64_t iters,
                         int64_t t_enter) {
     u64* r = R.open();
-    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) x.add(r, (u64)c.s.overlap_flags[i]);
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) R.add((u64)c.s.overlap_flags[i]);
     const u64 nov = R.close(r);
     if (x.leader()) {
         out->rebuilds = c.s.vl_meta[2] - rebuilds0;

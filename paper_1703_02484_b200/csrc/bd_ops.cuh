@@ -68,7 +68,7 @@ BD_HD void op_apply_crossings(X& x, Ctx& c, const int64_t* crossings) {
     u64* r = R.open();
     for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) {
         c.w.cross8[i] = (int8_t)crossings[i];
-        x.add(r, (u64)(crossings[i] != 0));
+        R.add((u64)(crossings[i] != 0));
     }
     if (R.close(r)) ph_apply_crossings(x, c);  // `if not np.any(crossings): return`
 }

@@ -143,6 +143,9 @@ enum {
     WK_T_TOTAL,        // ns from driver entry to exit
     WK_T_VERLET,       // ns in Verlet list rebuilds (cell sort + ordered pair fill)
     WK_T_SR_FORCE,     // ns in short-range force evaluations
+    WK_T_PRE,          // ns before the first integrate (force checks, SR force, rollback backup)
+    WK_T_INTEGRATE,    // ns in integrate + its apply_crossings
+    WK_PROBE0, WK_PROBE1, WK_PROBE2, WK_PROBE3,  // ns of finer sections (profiling aids)
     WK_N
 };
 
@@ -318,7 +321,7 @@ BD_HD u64 ph_integrate(X& x, Red<X>& R, Ctx& c, double dt, int64_t* cross64 = nu
             if (c.s.image) c.s.image[2 * i + k] += (int32_t)ci;
             crossed |= ci != 0;
         }
-        x.add(r, (u64)crossed);
+        R.add((u64)crossed);
     }
     return R.close(r);
 }
@@ -351,7 +354,7 @@ BD_HD bool ph_edge_inversion(X& x, Red<X>& R, Ctx& c) {
         const int64_t a = T.edge_v[2 * e], b = T.edge_v[2 * e + 1];
         const double d0x = mi_exact(prev[2 * b] - prev[2 * a], c.p), d0y = mi_exact(prev[2 * b + 1] - prev[2 * a + 1], c.p);
         const double d1x = mi_exact(cur[2 * b] - cur[2 * a], c.p), d1y = mi_exact(cur[2 * b + 1] - cur[2 * a + 1], c.p);
-        x.add(r, (u64)(d0x * d1x + d0y * d1y < 0.0));
+        R.add((u64)(d0x * d1x + d0y * d1y < 0.0));
     }
     return R.close(r) != 0;
 }
@@ -369,7 +372,7 @@ BD_HD u64 ph_inverted_tris(X& x, Red<X>& R, Ctx& c) {
         const double e2x = xy[2].x - xy[0].x, e2y = xy[2].y - xy[0].y;
         const bool inv = e1x * e2y - e1y * e2x <= 0.0;
         c.w.tinv[t] = (uint8_t)inv;
-        x.add(r, (u64)inv);
+        R.add((u64)inv);
     }
     return R.close(r);
 }
@@ -402,7 +405,7 @@ BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c) {
                 }
             }
             if (win) st[e] = ES_SEL;
-            x.add(rs, (u64)win);
+            R.add((u64)win);
         }
         nsel_total += R.close(rs);
         u64* ru = R.open();
@@ -420,7 +423,7 @@ BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c) {
                 }
             }
             if (blocked) st[e] = ES_REM;
-            x.add(ru, (u64)!blocked);
+            R.add((u64)!blocked);
         }
         if (R.close(ru) == 0) break;
     }
@@ -448,7 +451,7 @@ BD_HD int64_t restore_delaunay(X& x, Red<X>& R, Ctx& c, int64_t max_passes) {
             edge_quad(T, c.s.pos, c.p.L, e, q);
             const bool f = incircle(q[0], q[1], q[2], q[3], c.p.tol);
             c.w.estat[e] = f ? ES_UND : ES_NONE;
-            x.add(r, (u64)f);
+            R.add((u64)f);
         }
         if (R.close(r) == 0) return passes;
         passes++;
@@ -607,7 +610,7 @@ BD_HD int64_t correct_overlaps(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri) 
                 c.w.contrib[2 * e + 1] = delta * uy;
             }
             c.w.eovl[e] = (uint8_t)ov;
-            x.add(r, (u64)ov);
+            R.add((u64)ov);
         }
         if (R.close(r) == 0) return iterations;
         iterations++;
@@ -650,7 +653,7 @@ BD_HD int64_t correct_overlaps(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri) 
                 c.w.cross8[2 * i] = 0;
                 c.w.cross8[2 * i + 1] = 0;
             }
-            x.add(rc, (u64)crossed);
+            R.add((u64)crossed);
         }
         if (R.close(rc) && tri) ph_apply_crossings(x, c);
     }

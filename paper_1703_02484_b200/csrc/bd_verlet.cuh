@@ -98,12 +98,14 @@ template <class X>
 BD_HD bool vl_stale(X& x, Red<X>& R, Ctx& c) {
     if (x.ld((const u64*)&c.s.vl_meta[1]) == 0) return true;
     u64* r = R.open();
+    u64 m = 0;  // d2 >= 0: its bit pattern orders like the value
     for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
         const double dx = mi_exact(c.s.pos[2 * i] - c.s.vl_snap[2 * i], c.p);
         const double dy = mi_exact(c.s.pos[2 * i + 1] - c.s.vl_snap[2 * i + 1], c.p);
-        const double d2 = dx * dx + dy * dy;
-        x.umax(r, double_to_bits(d2));
+        const u64 b = double_to_bits(dx * dx + dy * dy);
+        m = b > m ? b : m;
     }
+    x.umax_all(r, m);  // one atomic per warp, not per particle
     const double worst = bits_to_double(R.close(r));
     const double h = c.p.skin / 2.0;
     return worst > h * h;

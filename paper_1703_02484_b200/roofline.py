@@ -54,13 +54,17 @@ PHASES = {  # pass kinds timed together (bd_stats_t.work timers)
     "incidence": (("incidence",), "t_incidence_ns"),
     "verlet": (("verlet_rebuild",), "t_verlet_ns"),
     "sr_force": (("sr_force",), "t_sr_force_ns"),
+    "pre": ((), "t_pre_ns"),
+    "integrate": (("integrate",), "t_integrate_ns"),
 }
 
 
 def phase_breakdown(work: dict) -> dict:
     """Share of the step kernel's time per phase group (device clock of the leader thread)."""
     tot = max(int(work.get("t_total_ns", 0)), 1)
-    out = {name: work.get(t, 0) / tot for name, (_, t) in PHASES.items()}
+    # the SR force and the Verlet rebuild it triggers run inside "pre" in the triangulation driver
+    out = {name: work.get(t, 0) / tot for name, (_, t) in PHASES.items() if name != "pre"}
+    out["pre"] = max(0.0, work.get("t_pre_ns", 0) - work.get("t_sr_force_ns", 0) - work.get("t_verlet_ns", 0)) / tot
     out["other"] = max(0.0, 1.0 - sum(out.values()))
     return out
 
