@@ -32,6 +32,8 @@ struct Ctl {
     u64 status;     // first error code (BD_ERR_*), 0 = ok
     u64 err_i, err_k;
     u64 scratch[5];
+    u64 lists[8];   // worklist lengths (restore_delaunay): two rings of 4
+    u64 gen;        // worklist dedup generation
     u64 bsum[4096]; // per-block partial sums (grid scans)
 };
 
@@ -108,6 +110,8 @@ struct ExecGrid {
     BD_DEV void umin(u64* p, u64 v) { atomicMin(p, v); }
     BD_DEV u64 cas(u64* p, u64 cmp, u64 v) { return atomicCAS(p, cmp, v); }
     BD_DEV int32_t fetch_add32(int32_t* p, int32_t v) { return atomicAdd(p, v); }
+    BD_DEV u64 fetch_add64(u64* p, u64 v) { return atomicAdd(p, v); }
+    BD_DEV uint32_t exch32(uint32_t* p, uint32_t v) { return atomicExch(p, v); }
     BD_DEV u64 ld(const u64* p) const { return ld_volatile(p); }
 
     // in-place exclusive scan of a[0..n) (int32), a[n] = total; ends with a barrier
@@ -154,6 +158,8 @@ struct ExecBlock {
     BD_DEV void umin(u64* p, u64 v) { atomicMin(p, v); }
     BD_DEV u64 cas(u64* p, u64 cmp, u64 v) { return atomicCAS(p, cmp, v); }
     BD_DEV int32_t fetch_add32(int32_t* p, int32_t v) { return atomicAdd(p, v); }
+    BD_DEV u64 fetch_add64(u64* p, u64 v) { return atomicAdd(p, v); }
+    BD_DEV uint32_t exch32(uint32_t* p, uint32_t v) { return atomicExch(p, v); }
     BD_DEV u64 ld(const u64* p) const { return ld_volatile(p); }
 
     BD_DEV void exclusive_scan(int32_t* a, int64_t n) {
@@ -198,6 +204,16 @@ struct ExecHost {
     int32_t fetch_add32(int32_t* p, int32_t v) {
         int32_t o = *p;
         *p += v;
+        return o;
+    }
+    u64 fetch_add64(u64* p, u64 v) {
+        u64 o = *p;
+        *p += v;
+        return o;
+    }
+    uint32_t exch32(uint32_t* p, uint32_t v) {
+        uint32_t o = *p;
+        *p = v;
         return o;
     }
     u64 ld(const u64* p) const { return *p; }

@@ -31,6 +31,9 @@ struct Ws {
     int32_t* inc_off;  // (n+1) CSR offsets of the overlap neighbour pairs per vertex
     int32_t* inc_cur;  // (n) fill cursors
     int32_t* inc;      // (2 items) incident pairs, ascending per vertex
+    int32_t* wl0;      // (ne) restore_delaunay worklist: flagged edges
+    int32_t* wl1;      // (ne) restore_delaunay worklist: edges to re-evaluate
+    uint32_t* stamp;   // (ne) worklist dedup stamps
     double* src4;      // all-pairs scratch (packed sources / sorted FAST workspace)
     // Verlet list (forces.py:67-156)
     int32_t* cell_id;    // (n)
@@ -52,7 +55,7 @@ BD_HD int64_t ncells_of(const bd_params_t& p) { return p.ncx > 0 ? p.ncx * p.ncx
 
 // layout of bd_workspace_bytes(); offsets relative to the workspace base
 struct WsLayout {
-    int64_t ctl, contrib, estat, eovl, tinv, cross8, image_bk, inc_off, inc_cur, inc, src4;
+    int64_t ctl, contrib, estat, eovl, tinv, cross8, image_bk, inc_off, inc_cur, inc, wl0, wl1, stamp, src4;
     int64_t cell_id, cell_start, cell_cur, corder, pcnt, vinc_off, vinc_cur, vinc, ov_idx, sr_err, sr_force, total;
 };
 
@@ -71,6 +74,9 @@ BD_HD WsLayout ws_layout(const bd_params_t& p, int64_t ne, int64_t nt) {
     l.inc_off = o; o = align_up(o + 4 * (n + 1));
     l.inc_cur = o; o = align_up(o + 4 * n);
     l.inc = o; o = align_up(o + 8 * items);
+    l.wl0 = o; o = align_up(o + 4 * ne);
+    l.wl1 = o; o = align_up(o + 4 * ne);
+    l.stamp = o; o = align_up(o + 4 * ne);
     // all-pairs scratch: packed double4 sources (EXACT) or the sorted FAST workspace
     {
         int64_t f = fast_ws_bytes(n) > 32 * n ? fast_ws_bytes(n) : 32 * n;
@@ -106,6 +112,9 @@ BD_HD Ws ws_carve(void* base, const bd_params_t& p, int64_t ne, int64_t nt) {
     w.inc_off = (int32_t*)(b + l.inc_off);
     w.inc_cur = (int32_t*)(b + l.inc_cur);
     w.inc = (int32_t*)(b + l.inc);
+    w.wl0 = (int32_t*)(b + l.wl0);
+    w.wl1 = (int32_t*)(b + l.wl1);
+    w.stamp = (uint32_t*)(b + l.stamp);
     w.src4 = (double*)(b + l.src4);
     w.cell_id = (int32_t*)(b + l.cell_id);
     w.cell_start = (int32_t*)(b + l.cell_start);
@@ -379,16 +388,21 @@ BD_HD u64 ph_inverted_tris(X& x, Red<X>& R, Ctx& c) {
 
 // lexicographically-first maximal independent set of the flagged edges
 // (== the reference's greedy ascending scan, triangulation.py:304-315),
-// then the flips of the selected edges.  Returns #flips.
+// then the flips of the selected edges.  Returns #flips.  The flagged edges
+// are list[0..m) when a list is given (restore_delaunay's worklist), else
+// every edge with estat == ES_UND; the result does not depend on the list
+// order (it is defined by the edge ids).
 template <class X>
-BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c) {
+BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c, const int32_t* list = nullptr, int64_t m = 0) {
     bd_tri_t& T = c.s.tri;
     uint8_t* st = c.w.estat;
+    const int64_t cnt = list ? m : T.ne;
     u64 nsel_total = 0;
     for (;;) {
         c.work[WK_LFMIS_ROUND]++;
         u64* rs = R.open();
-        for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+        for (int64_t j = x.tid(); j < cnt; j += x.nth()) {
+            const int64_t e = list ? list[j] : j;
             if (st[e] != ES_UND) continue;
             bool win = true;
             for (int side = 0; side < 2 && win; ++side) {
@@ -409,7 +423,8 @@ BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c) {
         }
         nsel_total += R.close(rs);
         u64* ru = R.open();
-        for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+        for (int64_t j = x.tid(); j < cnt; j += x.nth()) {
+            const int64_t e = list ? list[j] : j;
             if (st[e] != ES_UND) continue;
             bool blocked = false;
             for (int side = 0; side < 2 && !blocked; ++side) {
@@ -429,7 +444,8 @@ BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c) {
     }
     if (nsel_total == 0) return 0;
     c.work[WK_FLIPS] += (int64_t)nsel_total;
-    for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+    for (int64_t j = x.tid(); j < cnt; j += x.nth()) {
+        const int64_t e = list ? list[j] : j;
         if (st[e] != ES_SEL) continue;
         const int rc = flip_edge(T, e);
         if (rc) set_error(x, c, (u64)rc, e, 0);
@@ -438,30 +454,82 @@ BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c) {
     return nsel_total;
 }
 
-// restore_delaunay (triangulation.py:319-334); returns passes, or -1 on error
+// in-circle flag of edge e into estat; appends flagged edges to `out`
+template <class X>
+BD_HD bool flag_edge(X& x, Ctx& c, int64_t e, int32_t* out, u64* out_len) {
+    V2 q[4];
+    edge_quad(c.s.tri, c.s.pos, c.p.L, e, q);
+    const bool f = incircle(q[0], q[1], q[2], q[3], c.p.tol);
+    c.w.estat[e] = f ? ES_UND : ES_NONE;
+    if (f) out[x.fetch_add64(out_len, 1)] = (int32_t)e;
+    return f;
+}
+
+// restore_delaunay (triangulation.py:319-334); returns passes, or -1 on error.
+// The reference re-flags every edge each pass.  Positions do not move while
+// it runs, so after the first pass only the edges a flip can have changed
+// are re-evaluated: the flagged edges (flipped or not) and the boundary
+// edges of the flipped quads; every other edge keeps its (clear) flag.  The
+// per-pass flags, the flips and the pass count are the reference's.
 template <class X>
 BD_HD int64_t restore_delaunay(X& x, Red<X>& R, Ctx& c, int64_t max_passes) {
     bd_tri_t& T = c.s.tri;
+    u64* lens = c.w.ctl->lists;  // flagged-list lengths in lens[0..3], candidate lengths in lens[4..7]
+    int32_t* flagged = c.w.wl0;
+    int32_t* cand = c.w.wl1;
     int64_t passes = 0;
+    // pass 1 over every edge
+    c.work[WK_FLAG_PASS]++;
+    if (x.leader()) {
+        for (int k = 0; k < 8; ++k) lens[k] = 0;
+    }
+    x.sync();
+    const u64 gen0 = x.ld(&c.w.ctl->gen);  // stamps of this call: gen0 + 1, gen0 + 2, ...
+    u64* r = R.open();
+    for (int64_t e = x.tid(); e < T.ne; e += x.nth()) R.add((u64)flag_edge(x, c, e, flagged, &lens[0]));
+    u64 nflag = R.close(r);
     for (;;) {
-        c.work[WK_FLAG_PASS]++;
-        u64* r = R.open();
-        for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
-            V2 q[4];
-            edge_quad(T, c.s.pos, c.p.L, e, q);
-            const bool f = incircle(q[0], q[1], q[2], q[3], c.p.tol);
-            c.w.estat[e] = f ? ES_UND : ES_NONE;
-            R.add((u64)f);
+        if (nflag == 0) {
+            if (x.leader()) c.w.ctl->gen = gen0 + (u64)passes + 1;  // read again only after the next call's barrier
+            return passes;
         }
-        if (R.close(r) == 0) return passes;
         passes++;
         if (passes > max_passes) {
             set_error(x, c, BD_ERR_NONCONV, passes, 0);
             x.sync();
             return -1;
         }
-        ph_select_and_flip(x, R, c);
+        ph_select_and_flip(x, R, c, flagged, (int64_t)nflag);
         if (x.ld(&c.w.ctl->status)) return -1;
+        // candidates of the next pass (deduplicated by a per-call generation stamp)
+        const int ring = (int)(passes & 3);
+        u64* nc = &lens[4 + ring];
+        if (x.leader()) {
+            lens[4 + ((ring + 1) & 3)] = 0;  // reset the next rings before anyone appends to them
+            lens[(ring + 1) & 3] = 0;
+        }
+        const uint32_t gen = (uint32_t)(gen0 + (u64)passes);
+        for (int64_t j = x.tid(); j < (int64_t)nflag; j += x.nth()) {
+            const int64_t e = flagged[j];
+            const bool flipped = c.w.estat[e] == ES_SEL;
+            if (x.exch32(&c.w.stamp[e], gen) != gen) cand[x.fetch_add64(nc, 1)] = (int32_t)e;
+            if (!flipped) continue;
+            for (int side = 0; side < 2; ++side) {
+                const int64_t t = T.edge_tri[2 * e + side];
+                for (int k = 0; k < 3; ++k) {
+                    const int64_t f = T.tri_edge[3 * t + k];
+                    if (f != e && x.exch32(&c.w.stamp[f], gen) != gen) cand[x.fetch_add64(nc, 1)] = (int32_t)f;
+                }
+            }
+        }
+        x.sync();
+        const int64_t ncand = (int64_t)x.ld(nc);
+        // re-evaluate the candidates into the flagged list of the next pass
+        c.work[WK_FLAG_PASS]++;
+        u64* nf = &lens[(ring + 1) & 3];
+        r = R.open();
+        for (int64_t j = x.tid(); j < ncand; j += x.nth()) R.add((u64)flag_edge(x, c, cand[j], flagged, nf));
+        nflag = R.close(r);
     }
 }
 
