@@ -51,7 +51,7 @@ class BdStats(ctypes.Structure):
 WORK_KEYS = ("integrate", "apply_crossings", "edge_inversion", "flag_pass", "area_pass", "lfmis_round", "flips",
              "overlap_pass", "overlap_apply", "incidence", "verlet_rebuild", "sr_force",
              "t_maintain_ns", "t_overlap_ns", "t_incidence_ns", "t_total_ns", "t_verlet_ns", "t_sr_force_ns",
-             "t_pre_ns", "t_integrate_ns", "probe0", "probe1", "probe2", "probe3")
+             "t_pre_ns", "t_integrate_ns", "flag_edges_wl")
 
 
 STATS_WORDS = ctypes.sizeof(BdStats) // 8

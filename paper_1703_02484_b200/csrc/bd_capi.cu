@@ -336,6 +336,10 @@ void init_device_info() {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (const char* e = getenv("BD_WORKLIST_MIN_EDGES")) {
+            const int64_t v = atoll(e);
+            cudaMemcpyToSymbol(d_wl_min_edges, &v, sizeof(v));
+        }
         int m = occupancy((const void*)k_step_tri_grid<2>, STEP_BT);
         const void* coop[] = {(const void*)k_restore_delaunay_grid, (const void*)k_op_grid, (const void*)k_step_abp_grid<2>, (const void*)k_step_verlet_grid<2>,
                               (const void*)k_verlet_build_grid, (const void*)k_short_range_grid,

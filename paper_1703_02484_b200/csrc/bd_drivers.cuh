@@ -104,34 +104,26 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
     if (!driver_enter(x, R, c, out)) return;
     const int64_t rebuilds0 = c.s.vl_meta ? c.s.vl_meta[2] : 0;
     if (c.p.force_mode != BD_FORCE_SR && check_singular(x, R, c, c.s.force_err, out)) return;
-    int64_t tp = now_ns();
     if (c.p.force_mode != BD_FORCE_LR) {
         // short-range force over a Verlet list kept fresh by the rebuild rule
         const bool stale = vl_stale(x, R, c);
-        c.work[WK_PROBE0] = now_ns() - tp;
         if (stale && !vl_rebuild(x, R, c, 0.0)) {
             if (x.leader()) out->status = BD_ERR_CAPACITY;
             return;
         }
         sr_forces(x, c, c.w.sr_force, c.w.sr_err);
-        tp = now_ns();
         if (check_singular(x, R, c, c.w.sr_err, out)) return;
         const bool add = c.p.force_mode == BD_FORCE_LRSR;
         for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth())
             c.s.force[i] = add ? c.s.force[i] + c.w.sr_force[i] : c.w.sr_force[i];
         x.sync();
-        c.work[WK_PROBE1] = now_ns() - tp;
     }
-    tp = now_ns();
     if (check_finite(x, R, c, out)) return;
-    c.work[WK_PROBE2] = now_ns() - tp;
-    tp = now_ns();
     // save_state (triangulation.py:158-160) + image counters
     ph_tri_copy(x, c.s.tri, c.s.tri_backup);
     if (c.s.image)
         for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.w.image_bk[i] = c.s.image[i];
     x.sync();
-    c.work[WK_PROBE3] = now_ns() - tp;
 
     double dt_try = c.p.dt;
     int64_t rollbacks = 0, iters = 0, repairs = 0, flip_passes = 0;

@@ -154,7 +154,7 @@ enum {
     WK_T_SR_FORCE,     // ns in short-range force evaluations
     WK_T_PRE,          // ns before the first integrate (force checks, SR force, rollback backup)
     WK_T_INTEGRATE,    // ns in integrate + its apply_crossings
-    WK_PROBE0, WK_PROBE1, WK_PROBE2, WK_PROBE3,  // ns of finer sections (profiling aids)
+    WK_FLAG_EDGES_WL,  // edges re-evaluated by worklist passes of restore_delaunay
     WK_N
 };
 
@@ -471,9 +471,53 @@ BD_HD bool flag_edge(X& x, Ctx& c, int64_t e, int32_t* out, u64* out_len) {
 // are re-evaluated: the flagged edges (flipped or not) and the boundary
 // edges of the flipped quads; every other edge keeps its (clear) flag.  The
 // per-pass flags, the flips and the pass count are the reference's.
+// worklist passes cost two extra grid barriers per pass: below this many
+// edges the barriers dominate and every pass re-flags all edges instead
+// (cfg3: 0.79 vs 0.84 ms per step; cfg4, 3.1M edges: 3.71 vs 3.81 ms).
+// BD_WORKLIST_MIN_EDGES overrides (tests run both variants on the goldens).
+constexpr int64_t WORKLIST_MIN_EDGES = 1 << 20;
+#if defined(__CUDACC__)
+__device__ int64_t d_wl_min_edges = WORKLIST_MIN_EDGES;
+#endif
+BD_HD int64_t wl_min_edges() {
+#if defined(__CUDA_ARCH__)
+    return d_wl_min_edges;
+#else
+    const char* e = getenv("BD_WORKLIST_MIN_EDGES");  // host emulation: read per call
+    return e ? atoll(e) : WORKLIST_MIN_EDGES;
+#endif
+}
+
+template <class X>
+BD_HD int64_t restore_delaunay_full(X& x, Red<X>& R, Ctx& c, int64_t max_passes) {
+    bd_tri_t& T = c.s.tri;
+    int64_t passes = 0;
+    for (;;) {
+        c.work[WK_FLAG_PASS]++;
+        u64* r = R.open();
+        for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+            V2 q[4];
+            edge_quad(T, c.s.pos, c.p.L, e, q);
+            const bool f = incircle(q[0], q[1], q[2], q[3], c.p.tol);
+            c.w.estat[e] = f ? ES_UND : ES_NONE;
+            R.add((u64)f);
+        }
+        if (R.close(r) == 0) return passes;
+        passes++;
+        if (passes > max_passes) {
+            set_error(x, c, BD_ERR_NONCONV, passes, 0);
+            x.sync();
+            return -1;
+        }
+        ph_select_and_flip(x, R, c);
+        if (x.ld(&c.w.ctl->status)) return -1;
+    }
+}
+
 template <class X>
 BD_HD int64_t restore_delaunay(X& x, Red<X>& R, Ctx& c, int64_t max_passes) {
     bd_tri_t& T = c.s.tri;
+    if (T.ne < wl_min_edges()) return restore_delaunay_full(x, R, c, max_passes);
     u64* lens = c.w.ctl->lists;  // flagged-list lengths in lens[0..3], candidate lengths in lens[4..7]
     int32_t* flagged = c.w.wl0;
     int32_t* cand = c.w.wl1;
@@ -525,7 +569,7 @@ BD_HD int64_t restore_delaunay(X& x, Red<X>& R, Ctx& c, int64_t max_passes) {
         x.sync();
         const int64_t ncand = (int64_t)x.ld(nc);
         // re-evaluate the candidates into the flagged list of the next pass
-        c.work[WK_FLAG_PASS]++;
+        c.work[WK_FLAG_EDGES_WL] += ncand;
         u64* nf = &lens[(ring + 1) & 3];
         r = R.open();
         for (int64_t j = x.tid(); j < ncand; j += x.nth()) R.add((u64)flag_edge(x, c, cand[j], flagged, nf));

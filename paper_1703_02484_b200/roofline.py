@@ -20,6 +20,7 @@ PASS_BYTES = {
     "apply_crossings": lambda n, e, t, p, q: 30 * t + 2 * n,       # tri_v + shifts r/w, crossings
     "edge_inversion": lambda n, e, t, p, q: 8 * e + 32 * n,        # edge_v + prev/cur positions
     "flag_pass": lambda n, e, t, p, q: 11 * e + 18 * t + 16 * n,   # edge quad gather + flag write
+    "flag_edges_wl": lambda n, e, t, p, q: 11 + 36 + 32 + 8,       # per re-evaluated edge: quad, 4 positions, list
     "area_pass": lambda n, e, t, p, q: 19 * t + 16 * n,            # tri_v, shifts, positions, flag
     "lfmis_round": lambda n, e, t, p, q: 17 * e,                   # status of the edge + 4 neighbours
     "flips": lambda n, e, t, p, q: 190,                            # per flipped edge
@@ -49,7 +50,8 @@ def hbm_peak_gbs(measured: dict, default: float = 6538.6) -> float:
 
 
 PHASES = {  # pass kinds timed together (bd_stats_t.work timers)
-    "maintenance": (("edge_inversion", "flag_pass", "area_pass", "lfmis_round", "flips"), "t_maintain_ns"),
+    "maintenance": (("edge_inversion", "flag_pass", "flag_edges_wl", "area_pass", "lfmis_round", "flips"),
+                    "t_maintain_ns"),
     "overlap": (("overlap_pass", "overlap_apply", "apply_crossings"), "t_overlap_ns"),
     "incidence": (("incidence",), "t_incidence_ns"),
     "verlet": (("verlet_rebuild",), "t_verlet_ns"),

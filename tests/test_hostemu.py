@@ -106,8 +106,13 @@ class HostState:
                          self.work.nbytes)
 
 
+@pytest.mark.parametrize("worklist", [False, True], ids=["full-passes", "worklist"])
 @pytest.mark.parametrize("name", SCENARIOS)
-def test_host_driver_matches_reference(emu, name):
+def test_host_driver_matches_reference(emu, name, worklist, monkeypatch):
+    """Both restore_delaunay variants (every pass re-flags all edges / later
+    passes re-flag only the worklist; chosen by edge count, forced here)."""
+    if worklist:
+        monkeypatch.setenv("BD_WORKLIST_MIN_EDGES", "0")
     rec = load(name)
     fm = int(rec["force_mode"])
     verlet = str(rec["mode"]) == "verlet"
