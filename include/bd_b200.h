@@ -38,6 +38,7 @@ extern "C" {
 #define BD_ERR_STEPFAIL 4     /* StepFailure: non-finite force / rollback budget (dynamics.py:84-86, :254-258) */
 #define BD_ERR_FLIP 5         /* BrownsimError: unflippable edge (triangulation.py:261-280) */
 #define BD_ERR_CAPACITY 6     /* a device buffer (Verlet pairs) is too small: host grows it and retries */
+#define BD_ERR_BUILD 7        /* BuildError: no valid periodic triangulation (triangulation.py:545-550) */
 
 /* force models of one step: long range (dynamics.py:194),
  * short range over a Verlet list, or their sum F_LR + F_SR */
@@ -317,6 +318,19 @@ int bd_clear_status(const bd_state_t* s, void* stream);
 /* geometric audit counters (triangulation.py:386-482): out[0] = triangles
  * with area2 <= 0, out[1] = edges violating the in-circle test */
 int bd_tri_audit_geometry(const bd_state_t* s, const bd_params_t* p, int64_t* out, void* stream);
+
+/* Initial periodic Delaunay triangulation (build_initial /
+ * _build_from_tiling, triangulation.py:514-648) of the JITTERED points pos
+ * (n,2) on the torus [0,L)^2, written into out (out->nt = 2n triangles,
+ * out->ne = 3n edges, caller-allocated).  Same edge set as the reference's
+ * build on the same jittered points; indexing by owner vertex (see
+ * csrc/bd_build.cuh).  The caller then runs bd_tri_restore_delaunay on the
+ * unjittered points and audits, as the reference does.  result (device
+ * int64[4]) = {status (0 / BD_ERR_BUILD), vertex, reason, 0}; workspace of
+ * bd_tri_build_workspace_bytes(n, L) bytes. */
+int64_t bd_tri_build_workspace_bytes(int64_t n, double L);
+int bd_tri_build_initial(const double* pos, int64_t n, double L, const bd_tri_t* out, void* work, int64_t work_bytes,
+                         int64_t* result, void* stream);
 
 /* library version / build info (host) */
 const char* bd_build_info(void);

@@ -12,6 +12,7 @@ BD_ERR_NONCONV = 2
 BD_ERR_STEPFAIL = 4
 BD_ERR_FLIP = 5
 BD_ERR_CAPACITY = 6
+BD_ERR_BUILD = 7
 
 BD_FORCE_LR = 0
 BD_FORCE_SR = 1
@@ -112,6 +113,8 @@ def _protos():
         "bd_tri_restore_delaunay_ex": ([P(BdState), P(BdParams), c_i64, c_vp, c_vp], c_int),
         "bd_overlap_correct": ([P(BdState), P(BdParams), c_i64, c_int, c_vp, c_vp], c_int),
         "bd_tri_copy": ([P(BdTri), P(BdTri), c_vp], c_int),
+        "bd_tri_build_workspace_bytes": ([c_i64, c_d], c_i64),
+        "bd_tri_build_initial": ([c_vp, c_i64, c_d, P(BdTri), c_vp, c_i64, c_vp, c_vp], c_int),
         "bd_build_info": ([], ctypes.c_char_p),
     }
 
@@ -135,4 +138,5 @@ EXPORTS = ("bd_brute_overlaps", "bd_force","bd_force_prepare", "bd_force_slots",
            "bd_integrate", "bd_tri_apply_crossings", "bd_tri_edge_inversion", "bd_tri_signed_area2",
            "bd_tri_delaunay_flags", "bd_tri_inverted_edge_flags", "bd_tri_flip_edges", "bd_tri_repair_inversions",
            "bd_tri_restore_delaunay_ex", "bd_overlap_correct", "bd_tri_copy", "bd_step_abp", "bd_run_abp",
+           "bd_tri_build_workspace_bytes", "bd_tri_build_initial",
            "bd_long_range_workspace_bytes_for", "bd_force_sym_partial", "bd_force_sym_finish")

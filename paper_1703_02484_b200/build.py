@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "_lib", "libbd_b200.so")
 SOURCES = ["bd_capi.cu"]
 HEADERS = ["bd_common.cuh", "bd_exec.cuh", "bd_step.cuh", "bd_allpairs.cuh", "bd_allpairs_fast.cuh", "bd_verlet.cuh",
-           "bd_drivers.cuh", "bd_ops.cuh", "bd_allpairs_sym.cuh"]
+           "bd_drivers.cuh", "bd_ops.cuh", "bd_allpairs_sym.cuh", "bd_build.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [

@@ -12,6 +12,7 @@
 #include "bd_allpairs_sym.cuh"
 #include "bd_drivers.cuh"
 #include "bd_ops.cuh"
+#include "bd_build.cuh"
 
 using namespace bd;
 
@@ -290,6 +291,18 @@ __global__ void k_normals(uint64_t seed, uint64_t stream_id, uint64_t call, uint
     }
 }
 
+__global__ void __launch_bounds__(STEP_BT) k_tri_build_grid(const double* pos, int64_t n, double L, bd_tri_t out,
+                                                            void* work, int64_t* res) {
+    BuildCtx c;
+    c.g = build_geo(n, L);
+    c.w = build_carve(work, n, L);
+    c.pos = pos;
+    c.out = out;
+    ExecGrid x{c.w.ctl};
+    Poly P, Q;
+    tri_build(x, c, P, Q, res);
+}
+
 __global__ void k_audit_geometry(bd_tri_t T, const double* pos, double L, double tol, unsigned long long* out) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
     unsigned long long bad_area = 0, bad_circ = 0;
@@ -341,7 +354,7 @@ void init_device_info() {
             cudaMemcpyToSymbol(d_wl_min_edges, &v, sizeof(v));
         }
         int m = occupancy((const void*)k_step_tri_grid<2>, STEP_BT);
-        const void* coop[] = {(const void*)k_restore_delaunay_grid, (const void*)k_op_grid, (const void*)k_step_abp_grid<2>, (const void*)k_step_verlet_grid<2>,
+        const void* coop[] = {(const void*)k_restore_delaunay_grid, (const void*)k_op_grid, (const void*)k_tri_build_grid, (const void*)k_step_abp_grid<2>, (const void*)k_step_verlet_grid<2>,
                               (const void*)k_verlet_build_grid, (const void*)k_short_range_grid,
                               (const void*)k_overlap_pass_grid};
         for (const void* f : coop) {
@@ -926,6 +939,18 @@ int bd_tri_audit_geometry(const bd_state_t* s, const bd_params_t* p, int64_t* ou
     if (e != cudaSuccess) return err_code(e);
     k_audit_geometry<<<grid_for(s->tri.ne), 256, 0, st>>>(s->tri, s->pos, p->L, p->tol, (unsigned long long*)out);
     return err_code(cudaGetLastError());
+}
+
+int64_t bd_tri_build_workspace_bytes(int64_t n, double L) { return n > 0 ? build_layout(n, L).total : 0; }
+
+int bd_tri_build_initial(const double* pos, int64_t n, double L, const bd_tri_t* out, void* work, int64_t work_bytes,
+                         int64_t* result, void* stream) {
+    init_device_info();
+    if (n < 3 || work_bytes < build_layout(n, L).total) return -(int)cudaErrorInvalidValue;
+    cudaStream_t st = (cudaStream_t)stream;
+    bd_tri_t o = *out;
+    void* args[] = {(void*)&pos, (void*)&n, (void*)&L, (void*)&o, (void*)&work, (void*)&result};
+    return coop_launch((const void*)k_tri_build_grid, n, args, st);
 }
 
 // FP64 FMA throughput probe (roofline denominator, bench.py): 8 independent

@@ -9,8 +9,10 @@ read-out and validation (audit, canonical_edge_keys), as in the reference.
 build_initial() restates the reference's one-time construction
 (triangulation.py:514-648: jittered (2m+1)^2 tiling -> scipy Qhull ->
 quotient onto the torus) in vectorised numpy so it scales to 1M particles;
-its output arrays are identical to the reference's (tests/test_build.py).
+its output arrays are identical to the reference's (tests/test_setup_and_abi.py).
 The post-build Delaunay clean-up pass runs on the GPU.
+build_initial(method="device") builds the triangulation itself on the GPU
+(csrc/bd_build.cuh: per-point Voronoi cells by bisector clipping).
 """
 
 from __future__ import annotations
@@ -488,9 +490,7 @@ def build_initial_arrays(positions, box: PeriodicBox, tol: float = DEFAULT_TOL, 
         raise BuildError(f"need at least 3 points to triangulate, got {n}")
     if np.unique(pos, axis=0).shape[0] != n:
         raise BuildError("coincident points cannot be triangulated")
-    gen = np.random.Generator(np.random.Philox(key=np.array(_JITTER_KEY, dtype=np.uint64)))
-    jitter = gen.standard_normal((n, 2)) * (1e-9 * box.length)
-    jittered = pos + jitter
+    jittered = pos + build_jitter(n, box)
     last = ["no tiling produced a consistent quotient"]
     for margin in (1, 2, 3):
         arrays = build_from_tiling(jittered, box.length, n, margin)
@@ -507,12 +507,71 @@ def build_initial_arrays(positions, box: PeriodicBox, tol: float = DEFAULT_TOL, 
                      "degenerate for this box: " + "; ".join(last))
 
 
-def build_initial(positions, box: PeriodicBox, tol: float = DEFAULT_TOL, device=None) -> PeriodicTriangulation:
+def build_jitter(n: int, box: PeriodicBox) -> np.ndarray:
+    """The reference's build jitter (triangulation.py:536-540): 1e-9 L normals, fixed Philox key."""
+    gen = np.random.Generator(np.random.Philox(key=np.array(_JITTER_KEY, dtype=np.uint64)))
+    return gen.standard_normal((n, 2)) * (1e-9 * box.length)
+
+
+BUILD_REASONS = {1: "coincident points", 2: "Voronoi cell polygon overflow",
+                 3: "point set too sparse for the box (Voronoi cell not closed within half the box)",
+                 4: "Delaunay degree above 32", 5: "neighbour image beyond the adjacent box copy",
+                 6: "asymmetric neighbour relation (degenerate input)",
+                 7: "inconsistent triangle (degenerate input)",
+                 8: "repeated vertex in a triangle (too few points for the box)", 9: "Euler counts off"}
+
+
+def device_build_tensors(jittered, box: PeriodicBox, device=None) -> dict:
+    """The six arrays of the periodic Delaunay triangulation of `jittered`
+    (n,2), built on the GPU (bd_tri_build_initial, csrc/bd_build.cuh), as
+    device tensors.  Raises BuildError when the build fails."""
+    import torch
+    from ._lib import check, lib, require_cuda
+    from .dynamics import _stream, _tri_struct
+    require_cuda()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    pts = np.ascontiguousarray(jittered, dtype=np.float64)
+    n = pts.shape[0]
+    if n < 3:
+        raise BuildError(f"need at least 3 points to triangulate, got {n}")
+    L = float(box.length)
+    t = {k: torch.empty((m * n,) + _SHAPES[k], dtype=getattr(torch, np.dtype(_DTYPES[k]).name), device=dev)
+         for k, m in (("tri_v", 2), ("tri_shift", 2), ("tri_edge", 2), ("edge_v", 3), ("edge_tri", 3),
+                      ("edge_opp", 3))}
+    pos_t = torch.from_numpy(pts).to(dev)
+    wb = int(lib().bd_tri_build_workspace_bytes(n, L))
+    work = torch.empty(wb // 8 + 64, dtype=torch.int64, device=dev)
+    res = torch.zeros(4, dtype=torch.int64, device=dev)
+    ts = _tri_struct(t, n)
+    check(lib().bd_tri_build_initial(ctypes.c_void_p(pos_t.data_ptr()), n, L, ctypes.byref(ts),
+                                     ctypes.c_void_p(work.data_ptr()), work.numel() * 8,
+                                     ctypes.c_void_p(res.data_ptr()), _stream()), "bd_tri_build_initial")
+    status, vertex, reason, _ = (int(v) for v in res.cpu().numpy())
+    if status:
+        raise BuildError(f"device triangulation build failed at vertex {vertex}: "
+                         f"{BUILD_REASONS.get(reason, reason)}")
+    return t
+
+
+def build_initial(positions, box: PeriodicBox, tol: float = DEFAULT_TOL, device=None,
+                  method: str = "host") -> PeriodicTriangulation:
     """Periodic Delaunay triangulation of wrapped positions; the clean-up
-    flip pass (restore_delaunay) runs on the GPU."""
+    flip pass (restore_delaunay) runs on the GPU.
+
+    method="host": the reference's construction (Qhull on the jittered
+    tiling), array for array identical to the reference's -- trajectories
+    then match the reference bit for bit.  method="device": the whole build
+    on the GPU (csrc/bd_build.cuh, ~1000x faster, and it also succeeds where
+    the tiling fails); the same edge set as the reference's except where
+    Qhull mis-decides an exactly cocircular quad of the unjittered points
+    (both diagonals are Delaunay there), indexed by owner vertex."""
     from .dynamics import device_restore_delaunay
 
     pos = np.asarray(positions, dtype=np.float64)
+    if method == "device":
+        return build_initial_device(pos, box, tol, device)
+    if method != "host":
+        raise ValueError(f"unknown build method {method!r}")
 
     def restore(arrays):
         tri = PeriodicTriangulation(box, pos.shape[0], **arrays, tol=tol, device=device)
@@ -522,3 +581,36 @@ def build_initial(positions, box: PeriodicBox, tol: float = DEFAULT_TOL, device=
 
     arrays = build_initial_arrays(pos, box, tol, restore)
     return PeriodicTriangulation(box, pos.shape[0], **arrays, tol=tol, device=device)
+
+
+def build_initial_device(positions, box: PeriodicBox, tol: float = DEFAULT_TOL, device=None) -> PeriodicTriangulation:
+    """build_initial(method="device"): the reference's jitter, the device
+    Voronoi/Delaunay build, restore_delaunay on the unjittered points and
+    the geometric audit, all on the GPU (triangulation.py:514-550)."""
+    import torch
+    from ._lib import check, lib
+    from .dynamics import _stream, _tri_struct, device_restore_delaunay, make_params
+    from .core import SimParams
+    pos = np.asarray(positions, dtype=np.float64)
+    n = pos.shape[0]
+    if n >= 3 and np.unique(pos, axis=0).shape[0] != n:
+        raise BuildError("coincident points cannot be triangulated")
+    t = device_build_tensors(pos + build_jitter(n, box), box, device)
+    tri = PeriodicTriangulation(box, n, **t, tol=tol, device=device)
+    device_restore_delaunay(tri, pos, box, tol)
+    dev = tri.device
+    pos_t = torch.from_numpy(np.ascontiguousarray(pos)).to(dev)
+    out = torch.zeros(2, dtype=torch.int64, device=dev)
+    from ._abi import BdState
+    s = BdState()
+    s.pos = pos_t.data_ptr()
+    s.tri = _tri_struct(tri.tensors(), n)
+    bp = make_params(SimParams(n=n, sigma=1.0, dt=0.01, diffusion=0.0), box.length, 0, 0)
+    bp.tol = float(tol)
+    check(lib().bd_tri_audit_geometry(ctypes.byref(s), ctypes.byref(bp), ctypes.c_void_p(out.data_ptr()),
+                                      _stream()), "bd_tri_audit_geometry")
+    bad_area, bad_circle = (int(v) for v in out.cpu().numpy())
+    if bad_area or bad_circle:
+        raise BuildError(f"device build failed the audit: {bad_area} non-positive areas, "
+                         f"{bad_circle} in-circle violations")
+    return tri

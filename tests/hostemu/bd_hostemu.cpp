@@ -10,6 +10,7 @@
 #include "../../paper_1703_02484_b200/csrc/bd_allpairs.cuh"
 #include "../../paper_1703_02484_b200/csrc/bd_drivers.cuh"
 #include "../../paper_1703_02484_b200/csrc/bd_ops.cuh"
+#include "../../paper_1703_02484_b200/csrc/bd_build.cuh"
 
 using namespace bd;
 
@@ -105,6 +106,19 @@ void bdh_op(const bd_state_t* s, const bd_params_t* p, int64_t op, int64_t i0, i
         case 10: op_correct_overlaps(x, c, i0, i1 != 0, res); break;
         default: break;
     }
+}
+
+int64_t bdh_tri_build_workspace_bytes(int64_t n, double L) { return build_layout(n, L).total; }
+
+void bdh_tri_build(const double* pos, int64_t n, double L, const bd_tri_t* out, void* work, int64_t* res) {
+    BuildCtx c;
+    c.g = build_geo(n, L);
+    c.w = build_carve(work, n, L);
+    c.pos = pos;
+    c.out = *out;
+    ExecHost x{c.w.ctl};
+    static Poly P, Q;
+    tri_build(x, c, P, Q, res);
 }
 
 }  // extern "C"

@@ -37,7 +37,7 @@ C0 = [(0.5, 3.0, 3.0), (0.5, -3.0, -1.5)]
 CFGS = {
     1: dict(n=1024, rho=0.3, force="long-range", precision="exact", steps=100, seed=0),
     2: dict(n=16384, rho=0.3, force="short-range", precision="exact", steps=100, seed=0),
-    4: dict(n=1048576, rho=0.6, force="short-range", precision="exact", steps=20, seed=1),
+    4: dict(n=1048576, rho=0.6, force="short-range", precision="exact", steps=20, seed=1, build="device"),
     5: dict(n=65536, rho=0.3, force="long+short", precision="fast-sym", steps=10000, seed=0),
 }
 RESOLVE = 1.0 - 1e-9
@@ -53,7 +53,7 @@ def build(cfg):
     pos, types, alpha, mu = init_arrays(InitConfig(n=n, box=box, sigma=1.0, types=C0, seed=cfg["seed"]))
     t0 = time.perf_counter()
     sys_ = ParticleSystem(pos, types, alpha, mu, box)
-    tri = build_initial(sys_.positions, box)
+    tri = build_initial(sys_.positions, box, method=cfg.get("build", "host"))
     t_build = time.perf_counter() - t0
     r_cut = None if cfg["force"] == "long-range" else 2.5
     params = SimParams(n=n, sigma=1.0, dt=0.01, diffusion=0.01, r_cutoff=r_cut)
@@ -150,7 +150,7 @@ def run(cfg_id, args):
             "precision": cfg["precision"], "steps": K, "value": value, "unit": "particle-steps/s",
             "ms_per_step": dev_ms / K, "valid_every_checked_step": not bad, "checks": checks,
             "check_every": every, "overlap_scan": "brute" if brute else "cell-list", "violations": bad[:5],
-            "stats_total": stats_tot, "build_s": t_build, "cpu_baseline": cpu,
+            "stats_total": stats_tot, "build_s": t_build, "build": cfg.get("build", "host"), "cpu_baseline": cpu,
             "phase_ms": {"force": (dev_ms - maint_ms) / K, "maintain": maint_ms / K},
             "work_per_step": {k: v / K for k, v in work_tot.items()},
             "phases": phase_roofline({k: v / K for k, v in work_tot.items()}, n, ne, nt, pairs),
