@@ -37,6 +37,11 @@ from paper_1703_02484_b200.roofline import hbm_peak_gbs, phase_roofline, step_by
 
 C0 = [(0.5, 3.0, 3.0), (0.5, -3.0, -1.5)]
 FLOPS_PER_PAIR = 23  # algorithmic FP64 flops per directed pair (_kernels.py:48-56)
+# FP64 instructions the pair kernel's inner loop executes per DIRECTED pair (SASS of the hot loop;
+# DESIGN.md §3.1): fast-sym evaluates each unordered pair once (15.25 per unordered pair in the
+# factored uniform loop), fast is the directed kernel; each instruction takes one DFMA slot of the
+# FP64 pipe (2 flops at the measured peak)
+FP64_INST_PER_PAIR = {"fast-sym": 15.25 / 2, "fast": 12.0}
 
 
 def parse():
@@ -316,10 +321,12 @@ def run_ours(args):
                    "sample": f"failed: {exc}"}
     kname = {"fast-sym": "k_allpairs_sym", "fast": "k_allpairs_fast", "exact": "k_allpairs"}[args.precision]
     traffic, pipe = profiled_traffic(kname)
-    # kernels of ours per step: sort (4) + pack + pair kernel + partial sums + finish + unsort + rescan
-    # (fast-sym); sort (4) + pack + pair kernel + partition sums + unsort + rescan (fast); pack + pair
+    # kernels of ours per step: sort (4) + pack + tie check (5) + pair kernel + partial sums + finish +
+    # unsort + rescan (fast-sym); sort (4) + pack + pair kernel + partition sums + unsort + rescan (fast); pack + pair
     # kernel (+ slot copy in / out when sharded) (exact); then the persistent step kernel
-    launches_per_step = {"fast-sym": 11, "fast": 10, "exact": 3 if world == 1 else 5}[args.precision]
+    launches_per_step = {"fast-sym": 16, "fast": 10, "exact": 3 if world == 1 else 5}[args.precision]
+    inst = FP64_INST_PER_PAIR.get(args.precision)
+    hw = 2 * inst * pairs / (f_ms * 1e-3) / 1e12 if inst else None
     line = {
         "metric": "particle-steps/s (N x steps / s), long-range all-pairs + Delaunay maintenance + overlap correction",
         "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -339,12 +346,16 @@ def run_ours(args):
                      else "nominal 148x64x2x1.965GHz",
                      "kernel": kname, "flops_per_pair": FLOPS_PER_PAIR,
                      "fp64_pipe_active_pct_ncu": pipe,
+                     "fp64_inst_per_pair": inst,
+                     "hw_achieved": hw, "hw_frac": hw / peak if hw else None,
                      "note": "compute-bound FP64 kernel; achieved = 23 algorithmic flops per DIRECTED pair "
-                             "(the reference's arithmetic) over the device time of the whole force phase (sort, "
-                             "pack, pair kernel, combine); fast-sym executes 8 FP64 instructions per directed "
-                             "pair (one r^-3 per unordered pair) so the pipe utilisation from ncu is the "
-                             "hardware-side figure; traffic = DRAM bytes per launch of the pair kernel from the "
-                             "committed ncu --set full capture (profiles/)"},
+                             "(the reference's arithmetic, SURVEY 8(d)) over the device time of the whole force "
+                             "phase (sort, pack, tie check, pair kernel, combine). fast-sym evaluates each "
+                             "unordered pair once, so it needs fewer flops than that count and frac can exceed 1. "
+                             "hw_achieved is the hardware-side figure: the FP64 instructions the kernel executes "
+                             "(fp64_inst_per_pair, SASS) x 2 flops per DFMA slot over the same time; hw_frac is "
+                             "the fraction of the FP64 pipe it keeps busy. traffic = DRAM bytes per launch of "
+                             "the pair kernel from the committed ncu --set full capture (profiles/)"},
         "maintain_roofline": {
             "bound": "hbm", "kernel": "k_step_tri_grid (persistent O(N) step)",
             "achieved": float(np.sum(m_bytes) / (np.sum(m_ms) * 1e-3) / 1e9), "unit": "GB/s",

@@ -72,7 +72,7 @@ BD_HD int64_t fs_align(int64_t x) { return (x + 255) & ~(int64_t)255; }
 // bytes of the FAST-path scratch for n particles
 BD_HD int64_t fast_ws_bytes(int64_t n) {
     const int64_t nc = fast_ncells(n), nt = (n + FS_TS - 1) / FS_TS;
-    return fs_align(4 * n) + fs_align(4 * (nc + 1)) + fs_align(4 * nc) + fs_align(4 * n) + fs_align(48 * n) +
+    return fs_align(4 * n) + fs_align(4 * (2 * nc + 1)) + fs_align(8 * nc) + fs_align(4 * n) + fs_align(48 * n) +
            fs_align(32 * nt) + fs_align(24 * n) + fs_align(24 * n * fast_splits(n)) + 256;
 }
 
@@ -82,8 +82,8 @@ BD_HD SortWs fast_ws_carve(void* base, int64_t n) {
     SortWs w;
     w.grid_log2 = fast_grid_log2(n);
     w.cell_of = (int32_t*)b; b += fs_align(4 * n);
-    w.cell_off = (int32_t*)b; b += fs_align(4 * (nc + 1));
-    w.cell_cur = (int32_t*)b; b += fs_align(4 * nc);
+    w.cell_off = (int32_t*)b; b += fs_align(4 * (2 * nc + 1));  // 2 nc: FAST-SYM sorts by (group, cell)
+    w.cell_cur = (int32_t*)b; b += fs_align(8 * nc);
     w.order = (int32_t*)b; b += fs_align(4 * n);
     w.src = (Src6*)b; b += fs_align(48 * n);
     w.bbox = (uint64_t*)b; b += fs_align(32 * nt);
@@ -107,14 +107,20 @@ BD_HD uint32_t morton2(uint32_t x, uint32_t y) {
 
 #if defined(__CUDACC__)
 
-__global__ void k_sort_count(const double* __restrict__ pos, int64_t n, double L, SortWs w) {
+// group_alpha (FAST-SYM): particles whose alpha differs from alpha[0] sort
+// after all others -- cell keys c + G^2 -- so source tiles and receiver warps
+// carry one alpha (bd_allpairs_sym.cuh, factored pair evaluation)
+__global__ void k_sort_count(const double* __restrict__ pos, int64_t n, double L, SortWs w,
+                             const double* __restrict__ group_alpha = nullptr) {
     const int G = 1 << w.grid_log2;
     const double inv = (double)G / L;
+    const double a_ref = group_alpha ? group_alpha[0] : 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int cx = (int)(pos[2 * i] * inv), cy = (int)(pos[2 * i + 1] * inv);
         cx = cx < 0 ? 0 : (cx >= G ? G - 1 : cx);
         cy = cy < 0 ? 0 : (cy >= G ? G - 1 : cy);
-        const int c = (int)morton2((uint32_t)cx, (uint32_t)cy);
+        const int c = (int)morton2((uint32_t)cx, (uint32_t)cy) +
+                      ((group_alpha && !(group_alpha[i] == a_ref)) ? G * G : 0);
         w.cell_of[i] = c;
         atomicAdd(&w.cell_off[c], 1);
     }

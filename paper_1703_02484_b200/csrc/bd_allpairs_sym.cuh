@@ -46,7 +46,8 @@ struct alignas(16) SrcS {
 
 struct alignas(16) SelS {  // receiver image selector (axis_select of both axes)
     double cx_le, cx_gt, cy_le, cy_gt;
-    uint64_t Tx, Ty, amb, pad;
+    uint64_t Tx, Ty, amb;
+    uint64_t tie;  // bit 0 / 1: some source lies within eps of the x / y breakpoint (k_tie_check)
 };
 
 #ifndef BD_SY_CT
@@ -81,6 +82,10 @@ struct SymWs {
     SrcS* src;       // (n) sources in slot order
     SelS* sel;       // (n) receiver selectors in slot order
     uint64_t* bbox;  // (ntiles, 4) min/max bits of x and y per SY_TS tile
+    double* tile_a;  // (ntiles) the tile's alpha when all its sources share it, else NaN
+    int32_t* tcnt;   // (2 (n+1)) coordinate buckets (x, y): counts -> offsets (k_tie_*)
+    int32_t* tcur;   // (2 n) scatter cursors
+    double* tval;    // (2 n) coordinates by bucket
     double* apart;   // (SY_S, n, 2) receiver-side partial sums per chunk
     double* bpart;   // (D, n, 2) source-side partial sums per circulant distance
     double* slot3;   // (n, 3) fx, fy, flag per slot
@@ -90,6 +95,7 @@ struct SymWs {
 BD_HD int64_t sym_ws_bytes(int64_t n) {
     const int64_t D = sym_D(n) > 0 ? sym_D(n) : 1;
     return fast_ws_bytes(n) + fs_align(32 * n) + fs_align(64 * n) + fs_align(32 * sym_tiles(n)) +
+           fs_align(8 * sym_tiles(n)) + fs_align(8 * (n + 1)) + fs_align(8 * n) + fs_align(16 * n) +
            fs_align(16 * n * SY_S) + fs_align(16 * n * D) + fs_align(24 * n) + fs_align(16 * n) + 256;
 }
 
@@ -101,6 +107,10 @@ BD_HD SymWs sym_ws_carve(void* base, int64_t n) {
     w.src = (SrcS*)b; b += fs_align(32 * n);
     w.sel = (SelS*)b; b += fs_align(64 * n);
     w.bbox = (uint64_t*)b; b += fs_align(32 * sym_tiles(n));
+    w.tile_a = (double*)b; b += fs_align(8 * sym_tiles(n));
+    w.tcnt = (int32_t*)b; b += fs_align(8 * (n + 1));
+    w.tcur = (int32_t*)b; b += fs_align(8 * n);
+    w.tval = (double*)b; b += fs_align(16 * n);
     w.apart = (double*)b; b += fs_align(16 * n * SY_S);
     w.bpart = (double*)b; b += fs_align(16 * n * D);
     w.slot3 = (double*)b; b += fs_align(24 * n);
@@ -114,9 +124,9 @@ BD_HD SymWs sym_ws_carve(void* base, int64_t n) {
 __global__ void __launch_bounds__(SY_TS) k_sym_pack(const double* __restrict__ pos, const double* __restrict__ alpha,
                                                     const double* __restrict__ mu, int64_t n, double L, double lo,
                                                     double hi, SymWs w) {
-    __shared__ uint64_t red[4][SY_TS / 32];
+    __shared__ uint64_t red[6][SY_TS / 32];
     const int64_t s = (int64_t)blockIdx.x * SY_TS + threadIdx.x;
-    uint64_t xmin = ~0ull, xmax = 0, ymin = ~0ull, ymax = 0;
+    uint64_t xmin = ~0ull, xmax = 0, ymin = ~0ull, ymax = 0, amin = ~0ull, amax = 0;
     if (s < n) {
         const int64_t i = w.sort.order[s];
         const double x = pos[2 * i], y = pos[2 * i + 1];
@@ -135,10 +145,11 @@ __global__ void __launch_bounds__(SY_TS) k_sym_pack(const double* __restrict__ p
         q.Tx = sx.T;
         q.Ty = sy.T;
         q.amb = (uint64_t)(sx.amb || sy.amb);
-        q.pad = 0;
+        q.tie = 0;
         w.sel[s] = q;
         xmin = xmax = dbits(x);
         ymin = ymax = dbits(y);
+        amin = amax = dbits(r.a);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -146,6 +157,8 @@ __global__ void __launch_bounds__(SY_TS) k_sym_pack(const double* __restrict__ p
         xmax = max(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
         ymin = min(ymin, __shfl_xor_sync(0xffffffffu, ymin, o));
         ymax = max(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
+        amin = min(amin, __shfl_xor_sync(0xffffffffu, amin, o));
+        amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     }
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) {
@@ -153,6 +166,8 @@ __global__ void __launch_bounds__(SY_TS) k_sym_pack(const double* __restrict__ p
         red[1][wid] = xmax;
         red[2][wid] = ymin;
         red[3][wid] = ymax;
+        red[4][wid] = amin;
+        red[5][wid] = amax;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -161,12 +176,69 @@ __global__ void __launch_bounds__(SY_TS) k_sym_pack(const double* __restrict__ p
             xmax = max(xmax, red[1][k]);
             ymin = min(ymin, red[2][k]);
             ymax = max(ymax, red[3][k]);
+            amin = min(amin, red[4][k]);
+            amax = max(amax, red[5][k]);
         }
+        w.tile_a[blockIdx.x] = amin == amax ? bits_to_double(amin) : __longlong_as_double(0x7ff8000000000000ll);
         uint64_t* b = w.bbox + 4 * blockIdx.x;
         b[0] = xmin;
         b[1] = xmax;
         b[2] = ymin;
         b[3] = ymax;
+    }
+}
+
+// ---- which receivers can meet an image tie ----------------------------------
+// A pair is an image tie (source side's minimum image differs from the
+// receiver side's) only if the source coordinate lies within eps of the
+// receiver's breakpoint value (near_window).  Tiles whose box contains a
+// breakpoint need the exact source-side arithmetic (EDGE mode) only when
+// some source really is that close: one bucket pass over the coordinates
+// (n buckets per axis over [0, L)) flags those receivers, per axis.  In
+// lattice states many are flagged; once the particles have moved, none.
+
+BD_HD double sym_tie_eps(double L) { return L * 0x1p-44; }
+
+BD_DEV int64_t tie_bucket(double v, double L, int64_t B) {
+    int64_t b = (int64_t)(v / L * (double)B);
+    return b < 0 ? 0 : (b >= B ? B - 1 : b);
+}
+
+__global__ void k_tie_count(const double* __restrict__ pos, int64_t n, double L, SymWs w) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        atomicAdd(&w.tcnt[tie_bucket(pos[2 * i], L, n)], 1);
+        atomicAdd(&w.tcnt[n + 1 + tie_bucket(pos[2 * i + 1], L, n)], 1);
+    }
+}
+
+__global__ void k_tie_scatter(const double* __restrict__ pos, int64_t n, double L, SymWs w) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = pos[2 * i], y = pos[2 * i + 1];
+        const int64_t bx = tie_bucket(x, L, n), by = tie_bucket(y, L, n);
+        w.tval[w.tcnt[bx] + atomicAdd(&w.tcur[bx], 1)] = x;
+        w.tval[n + w.tcnt[n + 1 + by] + atomicAdd(&w.tcur[n + by], 1)] = y;
+    }
+}
+
+BD_DEV bool tie_axis(const SymWs& w, int64_t n, double L, uint64_t T, int axis) {
+    if (T == ~0ull) return false;
+    const double tv = bits_to_double(T), eps = sym_tie_eps(L);
+    const double lo_v = tv - eps > 0.0 ? tv - eps : 0.0, hi_v = tv + eps;
+    const uint64_t lo = dbits(lo_v), hi = dbits(hi_v);
+    const int32_t* off = w.tcnt + axis * (n + 1);
+    const double* val = w.tval + axis * n;
+    for (int64_t b = tie_bucket(lo_v, L, n); b <= tie_bucket(hi_v, L, n); ++b)
+        for (int32_t k = off[b]; k < off[b + 1]; ++k) {
+            const uint64_t v = dbits(val[k]);
+            if (v >= lo && v <= hi) return true;
+        }
+    return false;
+}
+
+__global__ void k_tie_check(int64_t n, double L, SymWs w) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        const SelS q = w.sel[s];
+        w.sel[s].tie = (uint64_t)tie_axis(w, n, L, q.Tx, 0) | ((uint64_t)tie_axis(w, n, L, q.Ty, 1) << 1);
     }
 }
 
@@ -187,8 +259,10 @@ BD_DEV double inv_r3(double r2) {
 struct SymRecv {
     double cx_le[SY_R], cx_gt[SY_R], cy_le[SY_R], cy_gt[SY_R];
     uint64_t Tx[SY_R], Ty[SY_R];
+    uint32_t tie[SY_R];  // SelS.tie
     double a[SY_R];   // alpha of the receiver (source-side factor); 0 for an inactive slot
     double ax[SY_R], ay[SY_R];  // receiver-side accumulators A
+    double sx[SY_R], sy[SY_R];  // factored tiles: sum of w d over the tile (A += alpha_tile s)
 };
 
 enum { SY_UNIFORM = 0, SY_SELECT = 1, SY_EDGE_M = 2, SY_GENERIC = 3 };
@@ -212,7 +286,12 @@ BD_DEV double raw_coord(double c_le, double c_gt, double L) { return c_gt < L ? 
 //   GENERIC -- exact min-image arithmetic on both sides (receivers within
 //              ulps of L/2 have ambiguous breakpoints; essentially never).
 
-template <int MODE>
+// FACT: the tile's sources share one alpha and the warp's receivers share
+// one alpha, so both factors leave the pair loop: the receiver side sums
+// w d per tile (scaled by the tile's alpha at its end), the source side sums
+// w d_src over the warp (scaled by the warp's alpha after the reduction).
+// 14 FP64 instructions per unordered pair instead of 16.
+template <int MODE, bool FACT = false>
 BD_DEV void sym_pair(SymRecv& r, const SrcS& s, const double* cx, const double* cy, const double* Ll, double& bx,
                      double& by) {
     double dx[SY_R], dy[SY_R];
@@ -239,12 +318,19 @@ BD_DEV void sym_pair(SymRecv& r, const SrcS& s, const double* cx, const double* 
             sym = -mi_fast(s.y - raw_coord(r.cy_le[m], r.cy_gt[m], Ll[0]), Ll[0], Ll[1], Ll[2]);
         }
         const double w = inv_r3(fma(dx[m], dx[m], dy[m] * dy[m]));
-        const double ta = s.a * w;
-        r.ax[m] = fma(ta, dx[m], r.ax[m]);
-        r.ay[m] = fma(ta, dy[m], r.ay[m]);
-        const double tb = r.a[m] * w;
-        bx = fma(tb, sxm, bx);
-        by = fma(tb, sym, by);
+        if (FACT) {
+            r.sx[m] = fma(w, dx[m], r.sx[m]);
+            r.sy[m] = fma(w, dy[m], r.sy[m]);
+            bx = fma(w, sxm, bx);
+            by = fma(w, sym, by);
+        } else {
+            const double ta = s.a * w;
+            r.ax[m] = fma(ta, dx[m], r.ax[m]);
+            r.ay[m] = fma(ta, dy[m], r.ay[m]);
+            const double tb = r.a[m] * w;
+            bx = fma(tb, sxm, bx);
+            by = fma(tb, sym, by);
+        }
     }
 }
 
@@ -307,16 +393,28 @@ BD_DEV double warp_sum(double v) {
 constexpr int SY_G = 8;  // sources per transposed reduction
 
 // a tile of `cnt` sources: pair evaluations + warp sums of the source side into bws[2*j .. 2*j+1]
-template <int MODE>
+// (FACT: ta = the tile's alpha, wa = the warp's receiver alpha)
+template <int MODE, bool FACT = false>
 BD_DEV void sym_tile(SymRecv& r, const SrcS* sm, int cnt, const double* cx, const double* cy, const double* Ll,
-                     double* bws, int lane) {
+                     double* bws, int lane, double ta = 0.0, double wa = 0.0) {
     int j = 0;
     const int g = (lane >> 2) & 7;  // this lane visits source j + (u ^ g) at step u
+    if (FACT) {
+#pragma unroll
+        for (int m = 0; m < SY_R; ++m) {
+            r.sx[m] = 0.0;
+            r.sy[m] = 0.0;
+        }
+    }
     for (; j + SY_G <= cnt; j += SY_G) {
         double bx[SY_G], by[SY_G];
 #pragma unroll
-        for (int u = 0; u < SY_G; ++u) sym_pair<MODE>(r, sm[j + (u ^ g)], cx, cy, Ll, bx[u], by[u]);
-        const double sx = tree8(bx), sy = tree8(by);
+        for (int u = 0; u < SY_G; ++u) sym_pair<MODE, FACT>(r, sm[j + (u ^ g)], cx, cy, Ll, bx[u], by[u]);
+        double sx = tree8(bx), sy = tree8(by);
+        if (FACT) {
+            sx *= wa;
+            sy *= wa;
+        }
         if ((lane & 3) == 0) {
             const int k = j + g;
             bws[2 * k] = sx;
@@ -325,11 +423,22 @@ BD_DEV void sym_tile(SymRecv& r, const SrcS* sm, int cnt, const double* cx, cons
     }
     for (; j < cnt; ++j) {
         double bx, by;
-        sym_pair<MODE>(r, sm[j], cx, cy, Ll, bx, by);
-        const double sx = warp_sum(bx), sy = warp_sum(by);
+        sym_pair<MODE, FACT>(r, sm[j], cx, cy, Ll, bx, by);
+        double sx = warp_sum(bx), sy = warp_sum(by);
+        if (FACT) {
+            sx *= wa;
+            sy *= wa;
+        }
         if (lane == 0) {
             bws[2 * j] = sx;
             bws[2 * j + 1] = sy;
+        }
+    }
+    if (FACT) {
+#pragma unroll
+        for (int m = 0; m < SY_R; ++m) {
+            r.ax[m] = fma(ta, r.sx[m], r.ax[m]);
+            r.ay[m] = fma(ta, r.sy[m], r.ay[m]);
         }
     }
 }
@@ -374,12 +483,19 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
         r.cy_gt[m] = q.cy_gt;
         r.Tx[m] = q.Tx;
         r.Ty[m] = q.Ty;
+        r.tie[m] = (uint32_t)q.tie;
         r.a[m] = act[m] ? w.src[sl].a : 0.0;
         r.ax[m] = 0.0;
         r.ay[m] = 0.0;
         amb |= act[m] && q.amb;
     }
     const double Ll[3] = {L, lo, hi};
+    // the warp's receivers all active with one alpha: factored tiles possible
+    const double wa = __shfl_sync(0xffffffffu, r.a[0], 0);
+    bool wone = true;
+#pragma unroll
+    for (int m = 0; m < SY_R; ++m) wone &= act[m] && r.a[m] == wa;
+    const bool wfact = __all_sync(0xffffffffu, wone);
 
     // this chunk's distances [d0, d1); chunk 0 adds the diagonal block (d = 0)
     const int64_t per = (D + SY_S - 1) / SY_S;
@@ -410,18 +526,21 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
         const bool use = !(even && d == D && d > 0 && I >= Mb / 2) && cnt > 0;
         const uint64_t* bb = w.bbox + 4 * t;
         const uint64_t bx0 = bb[0], bx1 = bb[1], by0 = bb[2], by1 = bb[3];
+        const double ta = w.tile_a[t];
+        const bool fact = wfact && ta == ta;  // NaN: mixed tile
         mbar_wait(&bars[st], (uint32_t)((qi >> 1) & 1));
         const SrcS* sm = tiles + st * SY_TS;
         double* bws = bw + ((size_t)st * SY_NW2 + wid) * SY_TS * 2;
         if (use) {
             double cx[SY_R], cy[SY_R];
             bool uni = true, edge = false;
-            const double eps = L * 0x1p-44;  // >> the ulps of L in which image ties live
+            const double eps = sym_tie_eps(L);  // >> the ulps of L in which image ties live
 #pragma unroll
             for (int m = 0; m < SY_R; ++m) {
                 const bool xle = bx1 <= r.Tx[m], xgt = bx0 > r.Tx[m], yle = by1 <= r.Ty[m], ygt = by0 > r.Ty[m];
                 uni &= (xle || xgt) && (yle || ygt);
-                edge |= near_window(bx0, bx1, r.Tx[m], eps) || near_window(by0, by1, r.Ty[m], eps);
+                edge |= ((r.tie[m] & 1) && near_window(bx0, bx1, r.Tx[m], eps)) ||
+                        ((r.tie[m] & 2) && near_window(by0, by1, r.Ty[m], eps));
                 cx[m] = xle ? r.cx_le[m] : r.cx_gt[m];
                 cy[m] = yle ? r.cy_le[m] : r.cy_gt[m];
             }
@@ -438,9 +557,15 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
             } else if (any_edge) {
                 sym_tile<SY_EDGE_M>(r, sm, cnt, cx, cy, Ll, bws, lane);
             } else if (all_uni) {
-                sym_tile<SY_UNIFORM>(r, sm, cnt, cx, cy, Ll, bws, lane);
+                if (fact)
+                    sym_tile<SY_UNIFORM, true>(r, sm, cnt, cx, cy, Ll, bws, lane, ta, wa);
+                else
+                    sym_tile<SY_UNIFORM>(r, sm, cnt, cx, cy, Ll, bws, lane);
             } else {
-                sym_tile<SY_SELECT>(r, sm, cnt, cx, cy, Ll, bws, lane);
+                if (fact)
+                    sym_tile<SY_SELECT, true>(r, sm, cnt, cx, cy, Ll, bws, lane, ta, wa);
+                else
+                    sym_tile<SY_SELECT>(r, sm, cnt, cx, cy, Ll, bws, lane);
             }
         }
         __syncthreads();  // stage st consumed; the warps' source-side sums of tile qi complete
