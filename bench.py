@@ -321,10 +321,10 @@ def run_ours(args):
                    "sample": f"failed: {exc}"}
     kname = {"fast-sym": "k_allpairs_sym", "fast": "k_allpairs_fast", "exact": "k_allpairs"}[args.precision]
     traffic, pipe = profiled_traffic(kname)
-    # kernels of ours per step: sort (4) + pack + tie check (5) + pair kernel + partial sums + finish +
+    # kernels of ours per step: sort (4) + pack + tie check (4) + pair kernel + partial sums + finish +
     # unsort + rescan (fast-sym); sort (4) + pack + pair kernel + partition sums + unsort + rescan (fast); pack + pair
     # kernel (+ slot copy in / out when sharded) (exact); then the persistent step kernel
-    launches_per_step = {"fast-sym": 16, "fast": 10, "exact": 3 if world == 1 else 5}[args.precision]
+    launches_per_step = {"fast-sym": 15, "fast": 10, "exact": 3 if world == 1 else 5}[args.precision]
     inst = FP64_INST_PER_PAIR.get(args.precision)
     hw = 2 * inst * pairs / (f_ms * 1e-3) / 1e12 if inst else None
     line = {

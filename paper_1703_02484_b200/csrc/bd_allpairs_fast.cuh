@@ -155,20 +155,30 @@ __global__ void __launch_bounds__(1024) k_sort_scan(SortWs w, int64_t ncells) {
     }
     __syncthreads();
     int64_t carry = seg[wid];
-    for (int64_t base = c0; base < c1; base += 32) {
-        const int64_t c = base + lane;
-        const int64_t v = c < c1 ? w.cell_off[c] : 0;
-        int64_t inc = v;
+    // 8 chunks of 32 loaded before they are scanned (the carry chain would
+    // otherwise serialise one global-load latency per chunk)
+    for (int64_t base = c0; base < c1; base += 8 * 32) {
+        int32_t v[8];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += t;
+        for (int u = 0; u < 8; ++u) {
+            const int64_t c = base + 32 * u + lane;
+            v[u] = c < c1 ? w.cell_off[c] : 0;
         }
-        if (c < c1) {
-            w.cell_off[c] = (int32_t)(carry + inc - v);
-            w.cell_cur[c] = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t c = base + 32 * u + lane;
+            int64_t inc = v[u];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            if (c < c1) {
+                w.cell_off[c] = (int32_t)(carry + inc - v[u]);
+                w.cell_cur[c] = 0;
+            }
+            carry += __shfl_sync(0xffffffffu, inc, 31);
         }
-        carry += __shfl_sync(0xffffffffu, inc, 31);
     }
 }
 

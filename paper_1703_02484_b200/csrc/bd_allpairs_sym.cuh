@@ -76,6 +76,7 @@ struct SymRange {
 
 BD_HD SymRange sym_range(int64_t n, int rank, int world);
 BD_HD int64_t sym_tiles(int64_t n) { return (n + SY_TS - 1) / SY_TS; }
+BD_HD int64_t sym_tie_buckets(int64_t n) { return n / 8 > 0 ? n / 8 : 1; }  // coordinate buckets per axis
 
 struct SymWs {
     SortWs sort;     // cell sort of the FAST path (order, cells); its src/bbox/part3 are unused here
@@ -83,9 +84,9 @@ struct SymWs {
     SelS* sel;       // (n) receiver selectors in slot order
     uint64_t* bbox;  // (ntiles, 4) min/max bits of x and y per SY_TS tile
     double* tile_a;  // (ntiles) the tile's alpha when all its sources share it, else NaN
-    int32_t* tcnt;   // (2 (n+1)) coordinate buckets (x, y): counts -> offsets (k_tie_*)
-    int32_t* tcur;   // (2 n) scatter cursors
-    double* tval;    // (2 n) coordinates by bucket
+    int32_t* tcnt;   // (2 B + 1) coordinate buckets (x then y, B = sym_tie_buckets): counts -> offsets
+    int32_t* tcur;   // (2 B) scatter cursors
+    double* tval;    // (2 n) coordinates by bucket (x values, then y values)
     double* apart;   // (SY_S, n, 2) receiver-side partial sums per chunk
     double* bpart;   // (D, n, 2) source-side partial sums per circulant distance
     double* slot3;   // (n, 3) fx, fy, flag per slot
@@ -95,7 +96,8 @@ struct SymWs {
 BD_HD int64_t sym_ws_bytes(int64_t n) {
     const int64_t D = sym_D(n) > 0 ? sym_D(n) : 1;
     return fast_ws_bytes(n) + fs_align(32 * n) + fs_align(64 * n) + fs_align(32 * sym_tiles(n)) +
-           fs_align(8 * sym_tiles(n)) + fs_align(8 * (n + 1)) + fs_align(8 * n) + fs_align(16 * n) +
+           fs_align(8 * sym_tiles(n)) + fs_align(4 * (2 * sym_tie_buckets(n) + 1)) +
+           fs_align(8 * sym_tie_buckets(n)) + fs_align(16 * n) +
            fs_align(16 * n * SY_S) + fs_align(16 * n * D) + fs_align(24 * n) + fs_align(16 * n) + 256;
 }
 
@@ -108,8 +110,8 @@ BD_HD SymWs sym_ws_carve(void* base, int64_t n) {
     w.sel = (SelS*)b; b += fs_align(64 * n);
     w.bbox = (uint64_t*)b; b += fs_align(32 * sym_tiles(n));
     w.tile_a = (double*)b; b += fs_align(8 * sym_tiles(n));
-    w.tcnt = (int32_t*)b; b += fs_align(8 * (n + 1));
-    w.tcur = (int32_t*)b; b += fs_align(8 * n);
+    w.tcnt = (int32_t*)b; b += fs_align(4 * (2 * sym_tie_buckets(n) + 1));
+    w.tcur = (int32_t*)b; b += fs_align(8 * sym_tie_buckets(n));
     w.tval = (double*)b; b += fs_align(16 * n);
     w.apart = (double*)b; b += fs_align(16 * n * SY_S);
     w.bpart = (double*)b; b += fs_align(16 * n * D);
@@ -204,30 +206,34 @@ BD_DEV int64_t tie_bucket(double v, double L, int64_t B) {
     return b < 0 ? 0 : (b >= B ? B - 1 : b);
 }
 
+// x buckets [0, B), y buckets [B, 2B): one scan gives both offset tables
 __global__ void k_tie_count(const double* __restrict__ pos, int64_t n, double L, SymWs w) {
+    const int64_t B = sym_tie_buckets(n);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        atomicAdd(&w.tcnt[tie_bucket(pos[2 * i], L, n)], 1);
-        atomicAdd(&w.tcnt[n + 1 + tie_bucket(pos[2 * i + 1], L, n)], 1);
+        atomicAdd(&w.tcnt[tie_bucket(pos[2 * i], L, B)], 1);
+        atomicAdd(&w.tcnt[B + tie_bucket(pos[2 * i + 1], L, B)], 1);
     }
 }
 
 __global__ void k_tie_scatter(const double* __restrict__ pos, int64_t n, double L, SymWs w) {
+    const int64_t B = sym_tie_buckets(n);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double x = pos[2 * i], y = pos[2 * i + 1];
-        const int64_t bx = tie_bucket(x, L, n), by = tie_bucket(y, L, n);
+        const int64_t bx = tie_bucket(x, L, B), by = B + tie_bucket(y, L, B);
         w.tval[w.tcnt[bx] + atomicAdd(&w.tcur[bx], 1)] = x;
-        w.tval[n + w.tcnt[n + 1 + by] + atomicAdd(&w.tcur[n + by], 1)] = y;
+        w.tval[w.tcnt[by] + atomicAdd(&w.tcur[by], 1)] = y;
     }
 }
 
 BD_DEV bool tie_axis(const SymWs& w, int64_t n, double L, uint64_t T, int axis) {
     if (T == ~0ull) return false;
+    const int64_t B = sym_tie_buckets(n);
     const double tv = bits_to_double(T), eps = sym_tie_eps(L);
     const double lo_v = tv - eps > 0.0 ? tv - eps : 0.0, hi_v = tv + eps;
     const uint64_t lo = dbits(lo_v), hi = dbits(hi_v);
-    const int32_t* off = w.tcnt + axis * (n + 1);
-    const double* val = w.tval + axis * n;
-    for (int64_t b = tie_bucket(lo_v, L, n); b <= tie_bucket(hi_v, L, n); ++b)
+    const int32_t* off = w.tcnt + axis * B;
+    const double* val = w.tval;
+    for (int64_t b = tie_bucket(lo_v, L, B); b <= tie_bucket(hi_v, L, B); ++b)
         for (int32_t k = off[b]; k < off[b + 1]; ++k) {
             const uint64_t v = dbits(val[k]);
             if (v >= lo && v <= hi) return true;

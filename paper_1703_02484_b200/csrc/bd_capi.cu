@@ -499,26 +499,28 @@ int launch_sym_partial(const double* pos, const double* alpha, const double* mu,
                        const SymWs& w, int rank, int world, double* part, cudaStream_t st) {
     init_device_info();
     if (n <= 0) return 0;
-    const int64_t nc = 2 * fast_ncells(n);  // (alpha group, Morton cell)
-    cudaError_t e = cudaMemsetAsync(w.sort.cell_off, 0, sizeof(int32_t) * (nc + 1), st);
+    // (alpha group, Morton cell) with ~8 particles per cell: tiles of 256
+    // slots stay as compact, and the single-CTA scan has 8x fewer cells
+    SortWs sw = w.sort;
+    sw.grid_log2 = sw.grid_log2 > 2 ? sw.grid_log2 - 1 : sw.grid_log2;
+    const int64_t nc = 2 * ((int64_t)1 << (2 * sw.grid_log2));
+    cudaError_t e = cudaMemsetAsync(sw.cell_off, 0, sizeof(int32_t) * (nc + 1), st);
     if (e != cudaSuccess) return err_code(e);
-    k_sort_count<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, w.sort, alpha);
-    k_sort_scan<<<1, 1024, 0, st>>>(w.sort, nc);
-    k_sort_scatter<<<grid_for(n), 256, 0, st>>>(n, w.sort);
-    k_sort_fix<<<grid_for(nc), 256, 0, st>>>(nc, w.sort);
+    k_sort_count<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, sw, alpha);
+    k_sort_scan<<<1, 1024, 0, st>>>(sw, nc);
+    k_sort_scatter<<<grid_for(n), 256, 0, st>>>(n, sw);
+    k_sort_fix<<<grid_for(nc), 256, 0, st>>>(nc, sw);
     k_sym_pack<<<(unsigned)sym_tiles(n), SY_TS, 0, st>>>(pos, alpha, mu, n, p.L, p.mi_lo, p.mi_hi, w);
     // receivers that can meet an image tie (EDGE mode only for those)
-    e = cudaMemsetAsync(w.tcnt, 0, sizeof(int32_t) * 2 * (n + 1), st);
+    const int64_t nb = 2 * sym_tie_buckets(n);
+    e = cudaMemsetAsync(w.tcnt, 0, sizeof(int32_t) * (nb + 1), st);
     if (e != cudaSuccess) return err_code(e);
     k_tie_count<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, w);
     {
-        SortWs tx = w.sort, ty = w.sort;
-        tx.cell_off = w.tcnt;
-        tx.cell_cur = w.tcur;
-        ty.cell_off = w.tcnt + n + 1;
-        ty.cell_cur = w.tcur + n;
-        k_sort_scan<<<1, 1024, 0, st>>>(tx, n);
-        k_sort_scan<<<1, 1024, 0, st>>>(ty, n);
+        SortWs tb = w.sort;
+        tb.cell_off = w.tcnt;
+        tb.cell_cur = w.tcur;
+        k_sort_scan<<<1, 1024, 0, st>>>(tb, nb);
     }
     k_tie_scatter<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, w);
     k_tie_check<<<grid_for(n), 256, 0, st>>>(n, p.L, w);
