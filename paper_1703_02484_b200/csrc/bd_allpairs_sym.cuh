@@ -15,18 +15,18 @@
 //
 // Work decomposition (deterministic: every sum has a fixed order):
 //  * slots are the Morton-sorted particles of the FAST path (same sort);
-//    receiver blocks I of SY_BT slots, one receiver per thread;
+//    receiver blocks I of SY_BT = 512 slots, SY_R = 4 receivers per lane;
 //  * block I pairs with blocks J = I + d (mod Mb), d = 1..D, D = Mb/2
 //    (circulant: every unordered block pair exactly once; for even Mb the
 //    d = D pairs belong to the lower block I < Mb/2), split into SY_S
 //    chunks of d -> grid (Mb, SY_S); chunk 0 also does the diagonal block
 //    J = I as directed pairs (receiver side only, k != i);
 //  * the source tiles of J (SY_TS slots) stream through shared memory by
-//    TMA; each lane owns two receivers, so every source feeds two pair
-//    evaluations; the lane's source-side partial (summed over its two
-//    receivers) is reduced over the warp by a butterfly (amortised over 64
-//    pairs), the CTA adds its warps in warp order and writes one partial
-//    per (d, source);
+//    TMA; each lane owns SY_R receivers, so every source feeds SY_R pair
+//    evaluations; the lane's source-side partial (summed over its
+//    receivers) is reduced over the warp by a transposed shuffle tree, the
+//    CTA adds its warps in warp order and writes one partial per
+//    (d, source);
 //  * k_sym_combine sums the SY_S receiver partials and the D source
 //    partials of every slot in fixed order: F = mu (A - B).
 // Multi-GPU: rank r of G owns the chunks [r S / G, (r+1) S / G) of every
@@ -50,10 +50,17 @@ struct alignas(16) SelS {  // receiver image selector (axis_select of both axes)
     uint64_t tie;  // bit 0 / 1: some source lies within eps of the x / y breakpoint (k_tie_check)
 };
 
+// 4 receivers per lane in CTAs of 4 warps, 3 CTAs per SM (<= 170
+// registers): 9.57 ms at cfg3 against 9.93 for 2 receivers in 8-warp CTAs at
+// 2 per SM (each source read from shared memory feeds 4 pair evaluations and
+// the source-side warp reduction is amortised over 32 pairs per lane)
 #ifndef BD_SY_CT
-#define BD_SY_CT 256
+#define BD_SY_CT 128
 #endif
-constexpr int SY_R = 2;                // receivers per lane
+#ifndef BD_SY_R
+#define BD_SY_R 4
+#endif
+constexpr int SY_R = BD_SY_R;          // receivers per lane
 constexpr int SY_CT = BD_SY_CT;        // threads per CTA
 constexpr int SY_BT = SY_CT * SY_R;    // receivers per block
 constexpr int SY_TS = 256;  // sources per shared-memory stage
@@ -61,7 +68,7 @@ constexpr int SY_TS = 256;  // sources per shared-memory stage
 #define BD_SY_S 64
 #endif
 #ifndef BD_SY_MINB
-#define BD_SY_MINB 2
+#define BD_SY_MINB 3
 #endif
 constexpr int SY_S = BD_SY_S;  // chunks of the circulant distance range (grid.y)
 
@@ -258,10 +265,10 @@ BD_DEV double inv_r3(double r2) {
     return y3 * fma(fma(1.875, e, 1.5), e, 1.0);
 }
 
-// Two receivers per lane (slots lane and lane + 32 of the warp's 64):
-// every source read from shared memory feeds two pair evaluations, and the
-// source-side partial of a lane is the sum over its two receivers before
-// the warp butterfly (so the reduction is amortised over 64 pairs).
+// SY_R receivers per lane (slots lane + 32 m of the warp's 32 SY_R): every
+// source read from shared memory feeds SY_R pair evaluations, and the
+// source-side partial of a lane is the sum over its receivers before the
+// warp reduction (so the reduction is amortised over 32 SY_R pairs).
 struct SymRecv {
     double cx_le[SY_R], cx_gt[SY_R], cy_le[SY_R], cy_gt[SY_R];
     uint64_t Tx[SY_R], Ty[SY_R];
@@ -460,7 +467,11 @@ BD_DEV void sym_issue(const SymWs& w, int64_t n, int64_t t, SrcS* tiles, uint64_
 
 constexpr int SY_NW2 = SY_CT / 32;   // warps per CTA
 // dynamic smem: 2 source stages + 2 buffers of per-warp source-side sums
-constexpr int SY_SMEM = 2 * SY_TS * (int)sizeof(SrcS) + 2 * SY_NW2 * SY_TS * 16;
+#ifndef BD_SY_NB
+#define BD_SY_NB 2
+#endif
+constexpr int SY_NB = BD_SY_NB;  // source-sum buffers (1: one more CTA barrier per tile, half the smem)
+constexpr int SY_SMEM = 2 * SY_TS * (int)sizeof(SrcS) + SY_NB * SY_NW2 * SY_TS * 16;
 
 // grid (Mb, SY_S), SY_CT threads; warp v of block I owns slots I*SY_BT + 64 v + {lane, lane + 32}
 __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int64_t n, double L, double lo, double hi,
@@ -479,7 +490,7 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
     bool act[SY_R], amb = false;
 #pragma unroll
     for (int m = 0; m < SY_R; ++m) {
-        slot[m] = I * SY_BT + 64 * wid + lane + 32 * m;
+        slot[m] = I * SY_BT + 32 * SY_R * wid + lane + 32 * m;
         act[m] = slot[m] < n;
         const int64_t sl = act[m] ? slot[m] : I * SY_BT;
         const SelS q = w.sel[sl];
@@ -536,7 +547,8 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
         const bool fact = wfact && ta == ta;  // NaN: mixed tile
         mbar_wait(&bars[st], (uint32_t)((qi >> 1) & 1));
         const SrcS* sm = tiles + st * SY_TS;
-        double* bws = bw + ((size_t)st * SY_NW2 + wid) * SY_TS * 2;
+        const int sb = SY_NB == 1 ? 0 : st;
+        double* bws = bw + ((size_t)sb * SY_NW2 + wid) * SY_TS * 2;
         if (use) {
             double cx[SY_R], cy[SY_R];
             bool uni = true, edge = false;
@@ -581,7 +593,7 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
         }
         if (use && d > 0) {
             // CTA sum of the warp sums (warp order) -> one partial per (d, source)
-            const double* bt = bw + (size_t)st * SY_NW2 * SY_TS * 2;
+            const double* bt = bw + (size_t)sb * SY_NW2 * SY_TS * 2;
             for (int e = threadIdx.x; e < 2 * cnt; e += SY_CT) {
                 double v = 0.0;
 #pragma unroll
@@ -590,6 +602,7 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
             }
         }
         // this stage's sum buffer is written again two tiles later, after the next __syncthreads
+        if (SY_NB == 1) __syncthreads();
     }
 #pragma unroll
     for (int m = 0; m < SY_R; ++m) {

@@ -10,6 +10,12 @@ from paper_1703_02484_b200 import build  # noqa: E402
 
 VARIANTS = {
     "sym_s64": ["BD_SY_S=64"],
+    "sym_r4_ct128_m3": ["BD_SY_R=4", "BD_SY_MINB=3", "BD_SY_CT=128"],
+    "sym_r6_ct128_m2": ["BD_SY_R=6", "BD_SY_MINB=2", "BD_SY_CT=128"],
+    "sym_r4_ct64_m6": ["BD_SY_R=4", "BD_SY_MINB=6", "BD_SY_CT=64"],
+    "sym_r4_ct64_m4": ["BD_SY_R=4", "BD_SY_MINB=4", "BD_SY_CT=64"],
+    "sym_r4_ct128_m3_s32": ["BD_SY_R=4", "BD_SY_MINB=3", "BD_SY_CT=128", "BD_SY_S=32"],
+    "sym_r4_ct128_m3_s128": ["BD_SY_R=4", "BD_SY_MINB=3", "BD_SY_CT=128", "BD_SY_S=128"],
 }
 
 if __name__ == "__main__":
