@@ -38,10 +38,10 @@ from paper_1703_02484_b200.roofline import hbm_peak_gbs, phase_roofline, step_by
 C0 = [(0.5, 3.0, 3.0), (0.5, -3.0, -1.5)]
 FLOPS_PER_PAIR = 23  # algorithmic FP64 flops per directed pair (_kernels.py:48-56)
 # FP64 instructions the pair kernel's inner loop executes per DIRECTED pair (SASS of the hot loop;
-# DESIGN.md §3.1): fast-sym evaluates each unordered pair once (15.25 per unordered pair in the
-# factored uniform loop), fast is the directed kernel; each instruction takes one DFMA slot of the
-# FP64 pipe (2 flops at the measured peak)
-FP64_INST_PER_PAIR = {"fast-sym": 15.25 / 2, "fast": 12.0}
+# DESIGN.md §3.1): fast-sym evaluates each unordered pair once (14.62 per unordered pair in the
+# factored uniform loop: 256 DFMA + 130 DMUL + 82 DADD per 8 sources x 4 receivers), fast is the
+# directed kernel; each instruction takes one DFMA slot of the FP64 pipe (2 flops at the measured peak)
+FP64_INST_PER_PAIR = {"fast-sym": 14.62 / 2, "fast": 12.0}
 
 
 def parse():
