@@ -31,6 +31,53 @@ def test_fast_sym_matches_exact_oracle(n):
     assert rel_err(out, ref) <= REL_TOL
 
 
+@pytest.mark.parametrize("n,table", [
+    (20000, [(2.0, 1.0), (0.0, 3.0), (-1.0, -2.0)]),     # three alphas, one of them 0
+    (9000, [(3.0, 3.0), (-3.0, -1.5)]),                  # c0: the factored path almost everywhere
+    (5000, [(-0.0, 1.0), (0.0, 2.0), (1.5, 1.0)]),       # -0 and +0 are different groups
+    (4099, [(1.0, 1.0)]),                                # one alpha: every tile factored
+])
+def test_fast_sym_alpha_groups(n, table):
+    """Factored tiles (slots sorted by alpha group: tiles / warps with one
+    alpha drop the per-pair charge products) and the mixed tiles at group
+    boundaries, against the exact oracle."""
+    from oracle import oracle as O
+    from paper_1703_02484_b200 import kernels
+    rng = np.random.default_rng(n)
+    L = float(np.sqrt(n * np.pi * 0.25 / 0.3))
+    pos = rng.uniform(0, L, size=(n, 2))
+    t = rng.integers(0, len(table), n)
+    alpha = np.array([a for a, _ in table])[t]
+    mu = np.array([m for _, m in table])[t]
+    ref, rerr = O.long_range(pos, alpha, mu, L)
+    out, err = kernels.long_range_kernel(pos, alpha, mu, L, precision="fast-sym")
+    assert np.array_equal(err, rerr)
+    nz = np.linalg.norm(ref, axis=1) > 0
+    assert rel_err(out[nz], ref[nz]) <= REL_TOL
+    assert np.abs(out[~nz]).max(initial=0.0) <= 1e-12
+
+
+def test_fast_sym_isolated_image_ties():
+    """A few exact half-box pairs in an otherwise random state: only the
+    receivers flagged by the coordinate-bucket tie check take the exact
+    source-side image (EDGE mode); everything else stays on the fast paths."""
+    from oracle import oracle as O
+    from paper_1703_02484_b200 import kernels
+    n = 6000
+    rng = np.random.default_rng(7)
+    L = float(np.sqrt(n * np.pi * 0.25 / 0.3))
+    pos = rng.uniform(0, L, size=(n, 2))
+    for i, j in ((5, 4000), (1234, 77), (2999, 3000), (5998, 10)):
+        pos[j, 0] = np.mod(pos[i, 0] + 0.5 * L, L)   # x exactly half a box apart
+    pos[4500, 1] = np.mod(pos[17, 1] - 0.5 * L, L)    # and one in y
+    t = rng.integers(0, 2, n)
+    alpha, mu = np.where(t == 0, 3.0, -3.0), np.where(t == 0, 3.0, -1.5)
+    ref, rerr = O.long_range(pos, alpha, mu, L)
+    out, err = kernels.long_range_kernel(pos, alpha, mu, L, precision="fast-sym")
+    assert np.array_equal(err, rerr)
+    assert rel_err(out, ref) <= REL_TOL
+
+
 @pytest.mark.parametrize("name", ["cfg1_lr_c0_n1024", "lr_c3_n512"])
 def test_fast_sym_lattice_states_with_exact_image_ties(name):
     """init_system's lattice states hold pairs at exactly L/2 (minimum-image
