@@ -53,6 +53,18 @@ BD_DEV void warp_atomic_add_u64(u64* p, u64 v) {
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(p, v);
 }
 
+// list append from possibly divergent code: the lanes that arrive together
+// take one atomic per warp and consecutive slots
+BD_DEV u64 warp_append(u64* counter) {
+    const unsigned mask = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    u64 base = 0;
+    if (lane == leader) base = atomicAdd(counter, (u64)__popc(mask));
+    base = __shfl_sync(mask, base, leader);
+    return base + (u64)__popc(mask & ((1u << lane) - 1u));
+}
+
 // max over the warp, one atomic per warp (every lane of the warp must call it)
 BD_DEV void warp_atomic_max_u64(u64* p, u64 v) {
 #pragma unroll
@@ -111,6 +123,7 @@ struct ExecGrid {
     BD_DEV u64 cas(u64* p, u64 cmp, u64 v) { return atomicCAS(p, cmp, v); }
     BD_DEV int32_t fetch_add32(int32_t* p, int32_t v) { return atomicAdd(p, v); }
     BD_DEV u64 fetch_add64(u64* p, u64 v) { return atomicAdd(p, v); }
+    BD_DEV u64 append(u64* p) { return warp_append(p); }  // list slot, one atomic per warp
     BD_DEV uint32_t exch32(uint32_t* p, uint32_t v) { return atomicExch(p, v); }
     BD_DEV u64 ld(const u64* p) const { return ld_volatile(p); }
 
@@ -159,6 +172,7 @@ struct ExecBlock {
     BD_DEV u64 cas(u64* p, u64 cmp, u64 v) { return atomicCAS(p, cmp, v); }
     BD_DEV int32_t fetch_add32(int32_t* p, int32_t v) { return atomicAdd(p, v); }
     BD_DEV u64 fetch_add64(u64* p, u64 v) { return atomicAdd(p, v); }
+    BD_DEV u64 append(u64* p) { return warp_append(p); }  // list slot, one atomic per warp
     BD_DEV uint32_t exch32(uint32_t* p, uint32_t v) { return atomicExch(p, v); }
     BD_DEV u64 ld(const u64* p) const { return ld_volatile(p); }
 
@@ -211,6 +225,7 @@ struct ExecHost {
         *p += v;
         return o;
     }
+    u64 append(u64* p) { return (*p)++; }
     uint32_t exch32(uint32_t* p, uint32_t v) {
         uint32_t o = *p;
         *p = v;

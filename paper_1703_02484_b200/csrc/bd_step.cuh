@@ -461,7 +461,7 @@ BD_HD bool flag_edge(X& x, Ctx& c, int64_t e, int32_t* out, u64* out_len) {
     edge_quad(c.s.tri, c.s.pos, c.p.L, e, q);
     const bool f = incircle(q[0], q[1], q[2], q[3], c.p.tol);
     c.w.estat[e] = f ? ES_UND : ES_NONE;
-    if (f) out[x.fetch_add64(out_len, 1)] = (int32_t)e;
+    if (f) out[x.append(out_len)] = (int32_t)e;
     return f;
 }
 
@@ -556,13 +556,13 @@ BD_HD int64_t restore_delaunay(X& x, Red<X>& R, Ctx& c, int64_t max_passes) {
         for (int64_t j = x.tid(); j < (int64_t)nflag; j += x.nth()) {
             const int64_t e = flagged[j];
             const bool flipped = c.w.estat[e] == ES_SEL;
-            if (x.exch32(&c.w.stamp[e], gen) != gen) cand[x.fetch_add64(nc, 1)] = (int32_t)e;
+            if (x.exch32(&c.w.stamp[e], gen) != gen) cand[x.append(nc)] = (int32_t)e;
             if (!flipped) continue;
             for (int side = 0; side < 2; ++side) {
                 const int64_t t = T.edge_tri[2 * e + side];
                 for (int k = 0; k < 3; ++k) {
                     const int64_t f = T.tri_edge[3 * t + k];
-                    if (f != e && x.exch32(&c.w.stamp[f], gen) != gen) cand[x.fetch_add64(nc, 1)] = (int32_t)f;
+                    if (f != e && x.exch32(&c.w.stamp[f], gen) != gen) cand[x.append(nc)] = (int32_t)f;
                 }
             }
         }
