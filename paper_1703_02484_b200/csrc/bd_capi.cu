@@ -48,6 +48,7 @@ int g_grid_blocks_per_sm = 0;
 int g_wide_blocks_per_sm = 0;
 int g_lr_blocks_per_sm[2] = {1, 1};
 int g_fast_blocks_per_sm = 1;
+int g_smem_optin = 0;  // max dynamic shared memory per CTA (opt-in)
 std::once_flag g_once;
 
 int64_t block_max_n() {
@@ -81,6 +82,89 @@ __global__ void __launch_bounds__(BLOCK_BT) k_step_tri_block(bd_state_t s, bd_pa
     Ctx c = make_ctx(s, p);
     ExecBlock x{c.w.ctl};
     step_tri_after_force(x, c, out);
+}
+
+// Small systems: the single-CTA driver keeps the triangulation, the
+// positions and the per-step scratch it gathers through (incidence lists,
+// flags, crossings) in shared memory for the whole step -- every phase is a
+// chain of dependent gathers and atomics, ~30 cycles each there instead of
+// ~600 from L2.  ~184 bytes per particle: N <= ~1200 within the 227 KB opt-in.
+struct SmemState {
+    int64_t tri_v, tri_shift, tri_edge, edge_v, edge_tri, edge_opp, pos, prev;
+    int64_t inc_off, inc_cur, inc, eovl, estat, cross8, tinv, total;
+};
+
+BD_HD int64_t al16(int64_t x) { return (x + 15) & ~(int64_t)15; }
+
+BD_HD SmemState smem_state(int64_t n, int64_t ne, int64_t nt) {
+    SmemState l;
+    int64_t o = 0;
+    l.tri_v = o; o = al16(o + 12 * nt);
+    l.tri_shift = o; o = al16(o + 6 * nt);
+    l.tri_edge = o; o = al16(o + 12 * nt);
+    l.edge_v = o; o = al16(o + 8 * ne);
+    l.edge_tri = o; o = al16(o + 8 * ne);
+    l.edge_opp = o; o = al16(o + 2 * ne);
+    l.pos = o; o = al16(o + 16 * n);
+    l.prev = o; o = al16(o + 16 * n);
+    l.inc_off = o; o = al16(o + 4 * (n + 1));
+    l.inc_cur = o; o = al16(o + 4 * n);
+    l.inc = o; o = al16(o + 8 * ne);
+    l.eovl = o; o = al16(o + ne);
+    l.estat = o; o = al16(o + ne);
+    l.cross8 = o; o = al16(o + 2 * n);
+    l.tinv = o; o = al16(o + nt);
+    l.total = o;
+    return l;
+}
+
+__device__ void blk_copy(void* dst, const void* src, int64_t bytes) {
+    const int64_t w = bytes >> 2;
+    for (int64_t i = threadIdx.x; i < w; i += blockDim.x) ((uint32_t*)dst)[i] = ((const uint32_t*)src)[i];
+    for (int64_t i = 4 * w + threadIdx.x; i < bytes; i += blockDim.x) ((uint8_t*)dst)[i] = ((const uint8_t*)src)[i];
+}
+
+__global__ void __launch_bounds__(BLOCK_BT) k_step_tri_block_smem(bd_state_t s, bd_params_t p, bd_stats_t* out) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int64_t n = p.n, ne = s.tri.ne, nt = s.tri.nt;
+    const SmemState l = smem_state(n, ne, nt);
+    bd_state_t ls = s;
+    ls.tri.tri_v = (int32_t*)(sm + l.tri_v);
+    ls.tri.tri_shift = (int8_t*)(sm + l.tri_shift);
+    ls.tri.tri_edge = (int32_t*)(sm + l.tri_edge);
+    ls.tri.edge_v = (int32_t*)(sm + l.edge_v);
+    ls.tri.edge_tri = (int32_t*)(sm + l.edge_tri);
+    ls.tri.edge_opp = (int8_t*)(sm + l.edge_opp);
+    ls.pos = (double*)(sm + l.pos);
+    ls.prev = (double*)(sm + l.prev);
+    blk_copy(ls.tri.tri_v, s.tri.tri_v, 12 * nt);
+    blk_copy(ls.tri.tri_shift, s.tri.tri_shift, 6 * nt);
+    blk_copy(ls.tri.tri_edge, s.tri.tri_edge, 12 * nt);
+    blk_copy(ls.tri.edge_v, s.tri.edge_v, 8 * ne);
+    blk_copy(ls.tri.edge_tri, s.tri.edge_tri, 8 * ne);
+    blk_copy(ls.tri.edge_opp, s.tri.edge_opp, 2 * ne);
+    blk_copy(ls.pos, s.pos, 16 * n);
+    blk_copy(ls.prev, s.prev, 16 * n);
+    __syncthreads();
+    Ctx c = make_ctx(ls, p);
+    c.w.inc_off = (int32_t*)(sm + l.inc_off);  // scratch: rebuilt / rewritten before every use
+    c.w.inc_cur = (int32_t*)(sm + l.inc_cur);
+    c.w.inc = (int32_t*)(sm + l.inc);
+    c.w.eovl = (uint8_t*)(sm + l.eovl);
+    c.w.estat = (uint8_t*)(sm + l.estat);
+    c.w.cross8 = (int8_t*)(sm + l.cross8);
+    c.w.tinv = (uint8_t*)(sm + l.tinv);
+    ExecBlock x{c.w.ctl};
+    step_tri_after_force(x, c, out);
+    __syncthreads();
+    blk_copy(s.tri.tri_v, ls.tri.tri_v, 12 * nt);
+    blk_copy(s.tri.tri_shift, ls.tri.tri_shift, 6 * nt);
+    blk_copy(s.tri.tri_edge, ls.tri.tri_edge, 12 * nt);
+    blk_copy(s.tri.edge_v, ls.tri.edge_v, 8 * ne);
+    blk_copy(s.tri.edge_tri, ls.tri.edge_tri, 8 * ne);
+    blk_copy(s.tri.edge_opp, ls.tri.edge_opp, 2 * ne);
+    blk_copy(s.pos, ls.pos, 16 * n);
+    blk_copy(s.prev, ls.prev, 16 * n);
 }
 
 template <int MINB>
@@ -373,6 +457,13 @@ void init_device_info() {
         g_lr_blocks_per_sm[0] = occupancy((const void*)k_allpairs<false>, LR_BT);
         g_fast_blocks_per_sm = occupancy((const void*)k_allpairs_fast, FS_BT);
         cudaFuncSetAttribute((const void*)k_allpairs_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, SY_SMEM);
+        cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        int st = 0;
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, (const void*)k_step_tri_block_smem) == cudaSuccess) st = (int)fa.sharedSizeBytes;
+        g_smem_optin -= st;
+        cudaFuncSetAttribute((const void*)k_step_tri_block_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             g_smem_optin);
     });
 }
 
@@ -585,7 +676,27 @@ int launch_driver(const void* grid_fn, const void* wide_fn, const void* block_fn
     return coop_launch(grid_fn, items, args, st, false, p->n < narrow_max_n() ? 1 : 0);
 }
 
+int64_t smem_driver_max_n() {  // BD_SMEM_DRIVER=0 turns the shared-memory single-CTA driver off
+    static int64_t v = -1;
+    if (v < 0) {
+        const char* e = getenv("BD_SMEM_DRIVER");
+        v = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    return v;
+}
+
 int launch_maintain_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
+    init_device_info();
+    if (p->n <= block_max_n() && smem_driver_max_n()) {
+        const int64_t bytes = smem_state(p->n, s->tri.ne, s->tri.nt).total;
+        if (bytes <= g_smem_optin) {
+            bd_state_t sv = *s;
+            bd_params_t pv = *p;
+            void* args[] = {&sv, &pv, &out};
+            return err_code(cudaLaunchKernel((const void*)k_step_tri_block_smem, dim3(1), dim3(BLOCK_BT), args,
+                                             (size_t)bytes, st));
+        }
+    }
     return launch_driver((const void*)k_step_tri_grid<2>, (const void*)k_step_tri_grid<WIDE_MINB>,
                          (const void*)k_step_tri_block, s, p, out, st);
 }
