@@ -63,7 +63,10 @@ struct alignas(16) SelS {  // receiver image selector (axis_select of both axes)
 constexpr int SY_R = BD_SY_R;          // receivers per lane
 constexpr int SY_CT = BD_SY_CT;        // threads per CTA
 constexpr int SY_BT = SY_CT * SY_R;    // receivers per block
-constexpr int SY_TS = 256;  // sources per shared-memory stage
+#ifndef BD_SY_TS
+#define BD_SY_TS 256
+#endif
+constexpr int SY_TS = BD_SY_TS;  // sources per shared-memory stage
 #ifndef BD_SY_S
 #define BD_SY_S 64
 #endif

@@ -9,13 +9,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1703_02484_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "sym_s64": ["BD_SY_S=64"],
+    "sym_ts128": ["BD_SY_TS=128"],
+    "sym_ts512": ["BD_SY_TS=512"],
     "sym_r4_ct128_m3": ["BD_SY_R=4", "BD_SY_MINB=3", "BD_SY_CT=128"],
-    "sym_r6_ct128_m2": ["BD_SY_R=6", "BD_SY_MINB=2", "BD_SY_CT=128"],
-    "sym_r4_ct64_m6": ["BD_SY_R=4", "BD_SY_MINB=6", "BD_SY_CT=64"],
-    "sym_r4_ct64_m4": ["BD_SY_R=4", "BD_SY_MINB=4", "BD_SY_CT=64"],
-    "sym_r4_ct128_m3_s32": ["BD_SY_R=4", "BD_SY_MINB=3", "BD_SY_CT=128", "BD_SY_S=32"],
-    "sym_r4_ct128_m3_s128": ["BD_SY_R=4", "BD_SY_MINB=3", "BD_SY_CT=128", "BD_SY_S=128"],
+    "sym_r2_m2_ct256": ["BD_SY_R=2", "BD_SY_MINB=2", "BD_SY_CT=256"],
 }
 
 if __name__ == "__main__":
