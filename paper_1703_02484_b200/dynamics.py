@@ -228,6 +228,21 @@ def _decode_stats(words: np.ndarray) -> dict:
     return d
 
 
+def _phase_ms(work: dict, force_ev_ms: float, drv_ms: float, tri: bool) -> tuple:
+    """StepStats (force_ms, maintain_ms, overlap_ms) with the reference's
+    meanings (dynamics.py:193-270, :328-341), from the device phase timers of
+    the step kernel (bd_stats_t.work, %globaltimer) and the force launch's
+    event time.  Triangulation steps: maintain = pass-through check +
+    inversion repair + Delaunay restoration, overlap = overlap rounds (with
+    their pair-incidence builds).  Verlet steps: maintain = list rebuild,
+    force = short-range force, overlap = integrate + overlap rounds."""
+    ns = lambda k: float(work.get(k, 0)) * 1e-6
+    if tri:
+        return force_ev_ms + ns("t_sr_force_ns"), ns("t_maintain_ns"), ns("t_overlap_ns") + ns("t_incidence_ns")
+    verlet, sr = ns("t_verlet_ns"), ns("t_sr_force_ns")
+    return sr, verlet, max(drv_ms - verlet - sr, 0.0)
+
+
 class _SimulationBase:
     """Shared run loop (dynamics.py:149-174); subclasses provide the launches."""
 
@@ -305,12 +320,13 @@ class _SimulationBase:
             drv_ms = evs[2 * j + 1].elapsed_time(evs[2 * j + 2])
             _raise_for(st, self.step_index)
             flags = self.last_overlap_flags.copy() if self.collect_flags else None
+            f_ms, m_ms, o_ms = _phase_ms(st["work"], force_ms if self._two_phase else 0.0, drv_ms,
+                                         self._two_phase)
             res.append(StepStats(step=self.step_index, dt_used=st["dt_used"],
                                  overlap_iterations=st["overlap_iterations"], flip_passes=st["flip_passes"],
                                  inversion_repairs=st["inversion_repairs"], rollbacks=st["rollbacks"],
-                                 n_overlapping=st["n_overlapping"],
-                                 force_ms=force_ms if self._two_phase else 0.0,
-                                 maintain_ms=drv_ms, overlap_ms=0.0, step_ms=force_ms + drv_ms, overlap_flags=flags,
+                                 n_overlapping=st["n_overlapping"], force_ms=f_ms, maintain_ms=m_ms,
+                                 overlap_ms=o_ms, step_ms=force_ms + drv_ms, overlap_flags=flags,
                                  work=st["work"]))
             self.step_index += 1
         return res
