@@ -284,7 +284,7 @@ def run_ours(args):
             sim.step()  # StepStats D2H inside (host sync)
             out_pos.copy_(sim.sys.positions_t, non_blocking=True)
             torch.cuda.synchronize()
-            host_pos.copy_(out_pos)
+            host_pos, out_pos = out_pos, host_pos  # this step's output is the next step's input
         dt = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([dt], dtype=torch.float64, device="cpu" if gloo_test else "cuda")

@@ -93,7 +93,8 @@ typedef struct bd_stats {
     int64_t overlap_iterations, flip_passes, inversion_repairs, rollbacks, n_overlapping;
     int64_t status, err_i, err_k;
     int64_t rebuilds; /* Verlet rebuilds during this step */
-    int64_t reserved[6];
+    int64_t calls;    /* noise-call counter after this step (CounterRng.call; *s->call) */
+    int64_t reserved[5];
     /* device work of the step, for the algorithmic-bytes roofline of the
      * O(N) path: passes of integrate, apply_crossings,
      * edge-inversion check, per-edge flag passes, per-triangle area passes,

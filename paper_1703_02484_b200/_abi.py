@@ -45,7 +45,7 @@ class BdStats(ctypes.Structure):
     _fields_ = [("dt_used", c_d), ("overlap_iterations", c_i64), ("flip_passes", c_i64),
                 ("inversion_repairs", c_i64), ("rollbacks", c_i64), ("n_overlapping", c_i64),
                 ("status", c_i64), ("err_i", c_i64), ("err_k", c_i64), ("rebuilds", c_i64),
-                ("reserved", c_i64 * 6), ("work", c_i64 * 24)]
+                ("calls", c_i64), ("reserved", c_i64 * 5), ("work", c_i64 * 24)]
 
 
 # bd_stats_t.work[] counters (csrc/bd_step.cuh WK_*)

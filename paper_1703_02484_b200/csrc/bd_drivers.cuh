@@ -192,6 +192,7 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
         out->status = (int64_t)c.w.ctl->status;
         out->err_i = (int64_t)c.w.ctl->err_i;
         out->err_k = (int64_t)c.w.ctl->err_k;
+        out->calls = (int64_t)c.call;
         c.work[WK_T_TOTAL] = now_ns() - t_enter;
         for (int k = 0; k < WK_N; ++k) out->work[k] = c.work[k];
         *c.s.call = c.call;
@@ -240,6 +241,7 @@ BD_HD void verlet_stats(X& x, Red<X>& R, Ctx& c, bd_stats_t* out, int64_t rebuil
         out->status = (int64_t)c.w.ctl->status;
         out->err_i = (int64_t)c.w.ctl->err_i;
         out->err_k = (int64_t)c.w.ctl->err_k;
+        out->calls = (int64_t)c.call;
         c.work[WK_T_TOTAL] = now_ns() - t_enter;
         for (int k = 0; k < WK_N; ++k) out->work[k] = c.work[k];
         *c.s.call = c.call;

@@ -310,10 +310,16 @@ class _SimulationBase:
             self._launch_driver(stats[j].data_ptr())
             evs[2 * j + 2].record()
         host = stats.cpu().numpy()
-        self.rng.call = int(self._eng.call_t.item())
+        decoded = [_decode_stats(host[j]) for j in range(steps)]
+        # the noise-call counter after the batch: from the last step's stats
+        # when every step ran clean (no second device read), else from HBM
+        if all(d["status"] == 0 for d in decoded):
+            self.rng.call = int(decoded[-1]["calls"])
+        else:
+            self.rng.call = int(self._eng.call_t.item())
         res = []
         for j in range(steps):
-            st = _decode_stats(host[j])
+            st = decoded[j]
             if st["status"] == -1:
                 break
             force_ms = evs[2 * j].elapsed_time(evs[2 * j + 1])
