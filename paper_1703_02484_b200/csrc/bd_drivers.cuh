@@ -92,8 +92,12 @@ BD_HD int64_t correct_overlaps_t(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri
 
 template <class X>
 BD_HD void build_edge_incidence_t(X& x, Ctx& c) {
+    // the lists depend on edge_v only, which only flips (and a rollback)
+    // change: an outer round whose maintenance flipped nothing reuses them
+    if (c.inc_flips == c.work[WK_FLIPS]) return;
     const int64_t t0 = now_ns();
     build_edge_incidence(x, c);
+    c.inc_flips = c.work[WK_FLIPS];
     c.work[WK_T_INCIDENCE] += now_ns() - t0;
 }
 
@@ -174,6 +178,7 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
         if (c.s.image)
             for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.s.image[i] = c.w.image_bk[i];
         ph_tri_copy(x, c.s.tri_backup, c.s.tri);
+        c.inc_flips = -1;  // edge_v restored: the incidence lists are stale
         x.sync();
         dt_try *= 0.5;
     }

@@ -166,10 +166,12 @@ struct Ctx {
     Ws w;
     uint64_t call;
     int64_t work[WK_N];
+    int64_t inc_flips;  // work[WK_FLIPS] when the edge incidence lists were last built (-1: stale)
 };
 
 BD_HD void ctx_init_work(Ctx& c) {
     for (int k = 0; k < WK_N; ++k) c.work[k] = 0;
+    c.inc_flips = -1;
 }
 
 // device wall clock (ns) for the phase breakdown; 0 on the host emulation
