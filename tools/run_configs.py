@@ -120,7 +120,7 @@ def run(cfg_id, args):
         res = sim.run(chunk)
         done += chunk
         dev_ms += sum(s.step_ms for s in res)
-        maint_ms += sum(s.maintain_ms for s in res)
+        maint_ms += sum(s.work["t_total_ns"] for s in res) * 1e-6  # the step kernel (O(N) path incl. SR force)
         pairs = int(sim._eng.vl_meta[0].item()) if cfg["force"] != "long-range" else 0
         mbytes += sum(step_bytes(s.work, n, ne, nt, pairs) for s in res)
         for s_ in res:
