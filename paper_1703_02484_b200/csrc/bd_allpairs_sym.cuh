@@ -620,17 +620,24 @@ __global__ void k_sym_partial(int64_t n, SymWs w, SymRange g, double* __restrict
     const int64_t Mb = sym_blocks(n), D = sym_D(n);
     const bool even = (Mb & 1) == 0;
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        // 16-byte loads, 8 in flight (the sums keep their sequential order)
         double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
+        const double2* ap = reinterpret_cast<const double2*>(w.apart) + s;
+#pragma unroll 8
         for (int c = g.c0; c < g.c1; ++c) {
-            ax += w.apart[(size_t)c * n * 2 + 2 * s];
-            ay += w.apart[(size_t)c * n * 2 + 2 * s + 1];
+            const double2 v = __ldcs(ap + (size_t)c * n);
+            ax += v.x;
+            ay += v.y;
         }
         const int64_t J = s / SY_BT;
-        for (int64_t d = g.d0; d < g.d1; ++d) {
-            const int64_t I = (J - d + Mb) % Mb;
-            if (even && d == D && I >= Mb / 2) continue;  // that pair was done by block J as receiver
-            bx += w.bpart[(size_t)(d - 1) * n * 2 + 2 * s];
-            by += w.bpart[(size_t)(d - 1) * n * 2 + 2 * s + 1];
+        // d = D of an even block count belongs to the lower block only
+        const int64_t dend = (even && g.d1 == D + 1 && (J - D + Mb) % Mb >= Mb / 2) ? D : g.d1;
+        const double2* bp = reinterpret_cast<const double2*>(w.bpart) + s;
+#pragma unroll 8
+        for (int64_t d = g.d0; d < dend; ++d) {
+            const double2 v = __ldcs(bp + (size_t)(d - 1) * n);
+            bx += v.x;
+            by += v.y;
         }
         part[2 * s] = ax - bx;
         part[2 * s + 1] = ay - by;
