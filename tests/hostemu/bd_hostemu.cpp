@@ -108,6 +108,15 @@ void bdh_op(const bd_state_t* s, const bd_params_t* p, int64_t op, int64_t i0, i
     }
 }
 
+// image selector of one coordinate (bd_allpairs.cuh axis_select): out = {T, shift_le, shift_gt, amb}
+void bdh_axis_select(double xi, double L, double lo, double hi, uint64_t* T, double* shifts, int* amb) {
+    const AxisSel a = axis_select(xi, L, lo, hi);
+    *T = a.T;
+    shifts[0] = a.shift_le;
+    shifts[1] = a.shift_gt;
+    *amb = a.amb;
+}
+
 int64_t bdh_tri_build_workspace_bytes(int64_t n, double L) { return build_layout(n, L).total; }
 
 void bdh_tri_build(const double* pos, int64_t n, double L, const bd_tri_t* out, void* work, int64_t* res) {

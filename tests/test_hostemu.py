@@ -48,6 +48,7 @@ def load_emu():
     lib.bdh_restore_delaunay.argtypes = [P(BdState), P(BdParams)]
     lib.bdh_restore_delaunay.restype = c_i64
     lib.bdh_step_abp.argtypes = [P(BdState), P(BdParams), P(BdStats)]
+    lib.bdh_axis_select.argtypes = [c_d, c_d, c_d, c_d, c_vp, c_vp, c_vp]
     _LIB = lib
     return lib
 
@@ -178,6 +179,38 @@ def test_min_image_breakpoints_exact(emu, L):
         d = float(d)
         if -L < d < L:
             assert emu.bdh_mi_fast(d, ctypes.byref(p)) == emu.bdh_mi_ref(d, L), d
+
+
+@pytest.mark.parametrize("L", [25.888345500742656, 17.0, 585.7893, 1171.5729, 3.0])
+def test_axis_select_breakpoint_is_the_bisection_result(emu, L):
+    """axis_select walks from s = x - thr to the breakpoint; it must return
+    exactly what a bisection over the bit patterns of [0, L) returns."""
+    p = params_for(emu, L)
+    smax = int(np.float64(L).view(np.uint64)) - 1
+    bits = lambda b: float(np.uint64(b).view(np.float64))
+    rng = np.random.default_rng(3)
+    xs = list(rng.uniform(0, L, 400)) + [0.0, np.nextafter(0, 1), L / 2, np.nextafter(L / 2, 0),
+                                         np.nextafter(L / 2, L), np.nextafter(L, 0), p.mi_hi, -p.mi_lo]
+    T, sh, amb = ctypes.c_uint64(), (ctypes.c_double * 2)(), ctypes.c_int()
+    for x in xs:
+        x = float(x)
+        emu.bdh_axis_select(x, L, p.mi_lo, p.mi_hi, ctypes.byref(T), sh, ctypes.byref(amb))
+        up, down = (x - 0.0) >= p.mi_hi, (x - bits(smax)) < p.mi_lo
+        if amb.value or not (up or down):
+            assert T.value == (1 << 64) - 1
+            continue
+        thr = p.mi_hi if up else p.mi_lo
+        good, bad = 0, smax + 1
+        if x - bits(smax) >= thr:
+            good = smax
+        else:
+            while bad - good > 1:
+                mid = (good + bad) // 2
+                if x - bits(mid) >= thr:
+                    good = mid
+                else:
+                    bad = mid
+        assert T.value == good, x
 
 
 @pytest.mark.parametrize("L", [25.888345500742656, 17.0, 585.7893, 414.2135623730951])
