@@ -22,7 +22,8 @@ constexpr int STEP_BT = 256;
 // The persistent step kernels exist twice: at <= 128 registers (2 CTAs per SM:
 // fewer, cheaper grid barriers -- best while barrier latency dominates) and
 // at 64 registers (4 CTAs per SM: twice the memory-level parallelism for the
-// dependent gathers of large N; 25 % faster at N = 1M, slower at 16k).
+// dependent gathers of large N; 25 % faster at N = 1M, 6 % at cfg3's 131k,
+// slower at 16k and 65k: wide from N = 100k).
 constexpr int WIDE_MINB = 4;
 int64_t lrw_max_n() {  // BD_LRW_MAX_N overrides the EXACT warp-per-receiver threshold (tuning)
     static int64_t v = -1;
@@ -37,7 +38,7 @@ int64_t wide_min_n() {  // BD_WIDE_MIN_N overrides (tests: the two variants must
     static int64_t v = -1;
     if (v < 0) {
         const char* e = getenv("BD_WIDE_MIN_N");
-        v = e ? atoll(e) : 200000;
+        v = e ? atoll(e) : 100000;
     }
     return v;
 }
