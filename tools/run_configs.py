@@ -37,6 +37,7 @@ C0 = [(0.5, 3.0, 3.0), (0.5, -3.0, -1.5)]
 CFGS = {
     1: dict(n=1024, rho=0.3, force="long-range", precision="exact", steps=100, seed=0),
     2: dict(n=16384, rho=0.3, force="short-range", precision="exact", steps=100, seed=0),
+    3: dict(n=131072, rho=0.3, force="long-range", precision="fast-sym", steps=1000, seed=0),  # long-run check
     4: dict(n=1048576, rho=0.6, force="short-range", precision="exact", steps=20, seed=1, build="device"),
     5: dict(n=65536, rho=0.3, force="long+short", precision="fast-sym", steps=10000, seed=0),
 }
@@ -100,7 +101,7 @@ def run(cfg_id, args):
         cfg["steps"] = args.steps
     sim, init, t_build = build(cfg)
     n, K = cfg["n"], cfg["steps"]
-    every = args.check_every or {1: 1, 2: 1, 4: 1, 5: 10}[cfg_id]
+    every = args.check_every or {1: 1, 2: 1, 3: 50, 4: 1, 5: 10}[cfg_id]
     brute = n <= 131072
     sim.run(3)  # warm-up (JIT-free, but first-touch / caches)
     torch.cuda.synchronize()
