@@ -112,3 +112,17 @@ def test_roofline_accounting_and_bench_imports():
         r = subprocess.run([sys.executable, os.path.join(ROOT, script), "--help"], capture_output=True, text=True,
                            timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_stepstats_phase_timings_follow_the_reference_meaning():
+    """StepStats force/maintain/overlap ms (dynamics.py:193-270, :328-341)
+    from the step kernel's device timers: triangulation steps split
+    maintenance from overlap rounds; Verlet steps report the list rebuild as
+    maintain and the short-range force as force."""
+    from paper_1703_02484_b200.dynamics import _phase_ms
+    work = {"t_maintain_ns": 300_000, "t_overlap_ns": 250_000, "t_incidence_ns": 50_000, "t_sr_force_ns": 20_000,
+            "t_verlet_ns": 40_000}
+    f, m, o = _phase_ms(work, 9.5, 0.8, True)
+    assert (round(f, 6), round(m, 6), round(o, 6)) == (9.52, 0.3, 0.3)
+    f, m, o = _phase_ms(work, 0.0, 0.5, False)
+    assert (round(f, 6), round(m, 6), round(o, 6)) == (0.02, 0.04, 0.44)
