@@ -677,7 +677,7 @@ int launch_driver(const void* grid_fn, const void* wide_fn, const void* block_fn
     return coop_launch(grid_fn, items, args, st, false, p->n < narrow_max_n() ? 1 : 0);
 }
 
-int64_t smem_driver_max_n() {  // BD_SMEM_DRIVER=0 turns the shared-memory single-CTA driver off
+int64_t smem_driver_enabled() {  // BD_SMEM_DRIVER=0 turns the shared-memory single-CTA driver off
     static int64_t v = -1;
     if (v < 0) {
         const char* e = getenv("BD_SMEM_DRIVER");
@@ -688,7 +688,7 @@ int64_t smem_driver_max_n() {  // BD_SMEM_DRIVER=0 turns the shared-memory singl
 
 int launch_maintain_tri(const bd_state_t* s, const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
     init_device_info();
-    if (p->n <= block_max_n() && smem_driver_max_n()) {
+    if (p->n <= block_max_n() && smem_driver_enabled()) {
         const int64_t bytes = smem_state(p->n, s->tri.ne, s->tri.nt).total;
         if (bytes <= g_smem_optin) {
             bd_state_t sv = *s;
