@@ -9,10 +9,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1703_02484_b200 import build  # noqa: E402
 
 VARIANTS = {
-    "sym_ts128": ["BD_SY_TS=128"],
-    "sym_ts512": ["BD_SY_TS=512"],
-    "sym_r4_ct128_m3": ["BD_SY_R=4", "BD_SY_MINB=3", "BD_SY_CT=128"],
-    "sym_r2_m2_ct256": ["BD_SY_R=2", "BD_SY_MINB=2", "BD_SY_CT=256"],
+    "sym_ct192_m2": ["BD_SY_CT=192", "BD_SY_MINB=2"],
+    "sym_ct256_m1": ["BD_SY_CT=256", "BD_SY_MINB=1"],
+    "sym_ct128_m3_s48": ["BD_SY_S=48"],
 }
 
 if __name__ == "__main__":
