@@ -394,8 +394,12 @@ BD_HD u64 ph_inverted_tris(X& x, Red<X>& R, Ctx& c) {
 // are list[0..m) when a list is given (restore_delaunay's worklist), else
 // every edge with estat == ES_UND; the result does not depend on the list
 // order (it is defined by the edge ids).
+// dirty/gen (restore_delaunay_full): every flipped edge and the four outer
+// edges of its quad -- the only edges whose quads a flip changes -- get
+// dirty[.] = gen
 template <class X>
-BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c, const int32_t* list = nullptr, int64_t m = 0) {
+BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c, const int32_t* list = nullptr, int64_t m = 0,
+                             uint32_t* dirty = nullptr, uint32_t gen = 0) {
     bd_tri_t& T = c.s.tri;
     uint8_t* st = c.w.estat;
     const int64_t cnt = list ? m : T.ne;
@@ -451,6 +455,13 @@ BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c, const int32_t* list = null
         if (st[e] != ES_SEL) continue;
         const int rc = flip_edge(T, e);
         if (rc) set_error(x, c, (u64)rc, e, 0);
+        if (dirty) {  // this flip's two triangles are touched by no other flip of the round
+            dirty[e] = gen;
+            for (int side = 0; side < 2; ++side) {
+                const int64_t t = T.edge_tri[2 * e + side];
+                for (int k = 0; k < 3; ++k) dirty[T.tri_edge[3 * t + k]] = gen;
+            }
+        }
     }
     x.sync();
     return nsel_total;
@@ -490,28 +501,44 @@ BD_HD int64_t wl_min_edges() {
 #endif
 }
 
+// Every pass re-flags every edge, but after the first only the edges a flip
+// touched (stamped by ph_select_and_flip) are re-tested: positions do not
+// move inside restore_delaunay, so every other edge keeps its quad and its
+// flag (flagged edges that were not flipped are ES_REM after selection).
+// Same flags, flips and pass counts as re-testing everything; no extra
+// barrier.
 template <class X>
 BD_HD int64_t restore_delaunay_full(X& x, Red<X>& R, Ctx& c, int64_t max_passes) {
     bd_tri_t& T = c.s.tri;
+    const u64 gen0 = x.ld(&c.w.ctl->gen);  // stamps of this call: gen0 + 1, gen0 + 2, ...
     int64_t passes = 0;
     for (;;) {
         c.work[WK_FLAG_PASS]++;
+        const uint32_t gen = (uint32_t)(gen0 + (u64)passes);
         u64* r = R.open();
         for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
-            V2 q[4];
-            edge_quad(T, c.s.pos, c.p.L, e, q);
-            const bool f = incircle(q[0], q[1], q[2], q[3], c.p.tol);
+            bool f;
+            if (passes == 0 || c.w.stamp[e] == gen) {
+                V2 q[4];
+                edge_quad(T, c.s.pos, c.p.L, e, q);
+                f = incircle(q[0], q[1], q[2], q[3], c.p.tol);
+            } else {
+                f = c.w.estat[e] != ES_NONE;
+            }
             c.w.estat[e] = f ? ES_UND : ES_NONE;
             R.add((u64)f);
         }
-        if (R.close(r) == 0) return passes;
+        if (R.close(r) == 0) {
+            if (x.leader()) c.w.ctl->gen = gen0 + (u64)passes + 1;  // read again only after the next call's barrier
+            return passes;
+        }
         passes++;
         if (passes > max_passes) {
             set_error(x, c, BD_ERR_NONCONV, passes, 0);
             x.sync();
             return -1;
         }
-        ph_select_and_flip(x, R, c);
+        ph_select_and_flip(x, R, c, nullptr, 0, c.w.stamp, (uint32_t)(gen0 + (u64)passes));
         if (x.ld(&c.w.ctl->status)) return -1;
     }
 }
