@@ -34,6 +34,7 @@ struct Ws {
     int32_t* wl0;      // (ne) restore_delaunay worklist: flagged edges
     int32_t* wl1;      // (ne) restore_delaunay worklist: edges to re-evaluate
     uint32_t* stamp;   // (ne) worklist dedup stamps
+    uint32_t* vhit;    // (n) correct_overlaps: sweep stamp of the particles with an overlapping pair
     double* src4;      // all-pairs scratch (packed sources / sorted FAST workspace)
     // Verlet list (forces.py:67-156)
     int32_t* cell_id;    // (n)
@@ -55,7 +56,7 @@ BD_HD int64_t ncells_of(const bd_params_t& p) { return p.ncx > 0 ? p.ncx * p.ncx
 
 // layout of bd_workspace_bytes(); offsets relative to the workspace base
 struct WsLayout {
-    int64_t ctl, contrib, estat, eovl, tinv, cross8, image_bk, inc_off, inc_cur, inc, wl0, wl1, stamp, src4;
+    int64_t ctl, contrib, estat, eovl, tinv, cross8, image_bk, inc_off, inc_cur, inc, wl0, wl1, stamp, vhit, src4;
     int64_t cell_id, cell_start, cell_cur, corder, pcnt, vinc_off, vinc_cur, vinc, ov_idx, sr_err, sr_force, total;
 };
 
@@ -77,6 +78,7 @@ BD_HD WsLayout ws_layout(const bd_params_t& p, int64_t ne, int64_t nt) {
     l.wl0 = o; o = align_up(o + 4 * ne);
     l.wl1 = o; o = align_up(o + 4 * ne);
     l.stamp = o; o = align_up(o + 4 * ne);
+    l.vhit = o; o = align_up(o + 4 * n);
     // all-pairs scratch: packed double4 sources (EXACT) or the sorted FAST workspace
     {
         int64_t f = fast_ws_bytes(n) > 32 * n ? fast_ws_bytes(n) : 32 * n;
@@ -115,6 +117,7 @@ BD_HD Ws ws_carve(void* base, const bd_params_t& p, int64_t ne, int64_t nt) {
     w.wl0 = (int32_t*)(b + l.wl0);
     w.wl1 = (int32_t*)(b + l.wl1);
     w.stamp = (uint32_t*)(b + l.stamp);
+    w.vhit = (uint32_t*)(b + l.vhit);
     w.src4 = (double*)(b + l.src4);
     w.cell_id = (int32_t*)(b + l.cell_id);
     w.cell_start = (int32_t*)(b + l.cell_start);
@@ -736,8 +739,12 @@ BD_HD int64_t correct_overlaps(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri) 
     double* pos = c.s.pos;
     const int64_t m = ps.count();
     int64_t iterations = 0;
+    // particles with an overlapping pair are stamped in the pass, so the
+    // apply gathers only theirs (the rest just clear their crossings)
+    const u64 g0 = x.ld(&c.w.ctl->vgen);
     for (int64_t it = 0; it < c.p.max_overlap_iters; ++it) {
         c.work[WK_OVL_PASS]++;
+        const uint32_t gen = (uint32_t)(g0 + 1 + (u64)it);
         u64* r = R.open();
         for (int64_t e = x.tid(); e < m; e += x.nth()) {
             const int64_t a = ps.a(e), b = ps.b(e);
@@ -749,15 +756,25 @@ BD_HD int64_t correct_overlaps(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri) 
                 const double ux = dx / rr, uy = dy / rr;
                 c.w.contrib[2 * e] = delta * ux;
                 c.w.contrib[2 * e + 1] = delta * uy;
+                c.w.vhit[a] = gen;
+                c.w.vhit[b] = gen;
             }
             c.w.eovl[e] = (uint8_t)ov;
             R.add((u64)ov);
         }
-        if (R.close(r) == 0) return iterations;
+        if (R.close(r) == 0) {
+            if (x.leader()) c.w.ctl->vgen = g0 + 2 + (u64)it;  // read again after the next call's barrier
+            return iterations;
+        }
         iterations++;
         c.work[WK_OVL_APPLY]++;
         u64* rc = R.open();
         for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
+            if (c.w.vhit[i] != gen) {
+                c.w.cross8[2 * i] = 0;
+                c.w.cross8[2 * i + 1] = 0;
+                continue;
+            }
             double dx = 0.0, dy = 0.0;
             bool hit = false;
             const int32_t j0 = c.w.inc_off[i], j1 = c.w.inc_off[i + 1];
@@ -798,6 +815,7 @@ BD_HD int64_t correct_overlaps(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri) 
         }
         if (R.close(rc) && tri) ph_apply_crossings(x, c);
     }
+    if (x.leader()) c.w.ctl->vgen = g0 + 2 + (u64)c.p.max_overlap_iters;
     set_error(x, c, BD_ERR_NONCONV, 0, 0);
     x.sync();
     return -1;
