@@ -711,14 +711,29 @@ BD_HD void build_incidence(X& x, int64_t n, const PS& ps, int32_t* off, int32_t*
     for (int64_t i = x.tid(); i < n; i += x.nth()) {
         int32_t* Lst = inc + off[i];
         const int32_t k = off[i + 1] - off[i];
+        if (k <= 16) {  // the usual case (Delaunay degree ~6): sort a private copy, one pass in, one out
+            int32_t v[16];
+            for (int32_t j = 0; j < k; ++j) v[j] = Lst[j];
+            for (int32_t j = 1; j < k; ++j) {
+                const int32_t t = v[j];
+                int32_t q = j - 1;
+                while (q >= 0 && v[q] > t) {
+                    v[q + 1] = v[q];
+                    --q;
+                }
+                v[q + 1] = t;
+            }
+            for (int32_t j = 0; j < k; ++j) Lst[j] = v[j];
+            continue;
+        }
         for (int32_t j = 1; j < k; ++j) {
-            const int32_t v = Lst[j];
+            const int32_t t = Lst[j];
             int32_t q = j - 1;
-            while (q >= 0 && Lst[q] > v) {
+            while (q >= 0 && Lst[q] > t) {
                 Lst[q + 1] = Lst[q];
                 --q;
             }
-            Lst[q + 1] = v;
+            Lst[q + 1] = t;
         }
     }
     x.sync();
