@@ -194,6 +194,21 @@ __global__ void k_sort_fix(int64_t ncells, SortWs w) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncells; c += (int64_t)gridDim.x * blockDim.x) {
         int32_t* a = w.order + w.cell_off[c];
         const int32_t m = w.cell_off[c + 1] - w.cell_off[c];
+        if (m <= 24) {  // the usual case: sort a private copy (one pass in, one out)
+            int32_t v[24];
+            for (int32_t j = 0; j < m; ++j) v[j] = a[j];
+            for (int32_t j = 1; j < m; ++j) {
+                const int32_t t = v[j];
+                int32_t k = j - 1;
+                while (k >= 0 && v[k] > t) {
+                    v[k + 1] = v[k];
+                    --k;
+                }
+                v[k + 1] = t;
+            }
+            for (int32_t j = 0; j < m; ++j) a[j] = v[j];
+            continue;
+        }
         for (int32_t j = 1; j < m; ++j) {
             const int32_t v = a[j];
             int32_t k = j - 1;
