@@ -158,6 +158,21 @@ BD_HD bool vl_rebuild_impl(X& x, Red<X>& R, Ctx& c, double margin) {
         for (int64_t k = x.tid(); k < nc; k += x.nth()) {
             int32_t* a = c.w.corder + c.w.cell_start[k];
             const int32_t m = c.w.cell_start[k + 1] - c.w.cell_start[k];
+            if (m <= 24) {  // the usual case: sort a private copy (one pass in, one out)
+                int32_t v[24];
+                for (int32_t j = 0; j < m; ++j) v[j] = a[j];
+                for (int32_t j = 1; j < m; ++j) {
+                    const int32_t t = v[j];
+                    int32_t q = j - 1;
+                    while (q >= 0 && v[q] > t) {
+                        v[q + 1] = v[q];
+                        --q;
+                    }
+                    v[q + 1] = t;
+                }
+                for (int32_t j = 0; j < m; ++j) a[j] = v[j];
+                continue;
+            }
             for (int32_t j = 1; j < m; ++j) {
                 const int32_t v = a[j];
                 int32_t q = j - 1;
