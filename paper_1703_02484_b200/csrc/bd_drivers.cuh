@@ -15,9 +15,7 @@ namespace bd {
 // first receiver with a non-zero err sentinel -> SingularityError (forces.py:54-58)
 template <class X>
 BD_HD bool check_singular(X& x, Red<X>& R, Ctx& c, const int64_t* err, bd_stats_t* out) {
-    u64* r = R.open();
-    if (x.leader()) c.w.ctl->scratch[1] = ~0ull;
-    x.sync();
+    u64* r = R.open();  // scratch[1] = ~0 since driver_enter / op_enter (only an error, which ends the step, lowers it)
     for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
         const bool bad = err[i] != 0;
         if (bad) x.umin(&c.w.ctl->scratch[1], (u64)i);
@@ -40,9 +38,7 @@ BD_HD bool check_singular(X& x, Red<X>& R, Ctx& c, const int64_t* err, bd_stats_
 // non-finite force -> StepFailure (integrate, dynamics.py:84-86)
 template <class X>
 BD_HD bool check_finite(X& x, Red<X>& R, Ctx& c, bd_stats_t* out) {
-    u64* r = R.open();
-    if (x.leader()) c.w.ctl->scratch[0] = ~0ull;
-    x.sync();
+    u64* r = R.open();  // scratch[0] = ~0 since driver_enter / op_enter
     for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
         const bool bad = !(isfinite(c.s.force[2 * i]) && isfinite(c.s.force[2 * i + 1]));
         if (bad) x.umin(&c.w.ctl->scratch[0], (u64)i);
@@ -61,8 +57,11 @@ BD_HD bool check_finite(X& x, Red<X>& R, Ctx& c, bd_stats_t* out) {
 
 template <class X>
 BD_HD bool driver_enter(X& x, Red<X>& R, Ctx& c, bd_stats_t* out) {
-    if (x.leader())
+    if (x.leader()) {
         for (int k = 0; k < 8; ++k) c.w.ctl->red[k] = 0;
+        c.w.ctl->scratch[0] = ~0ull;  // first bad index of check_finite / check_singular
+        c.w.ctl->scratch[1] = ~0ull;
+    }
     x.sync();
     if (x.ld(&c.w.ctl->status)) {  // an earlier step failed: this one does not run
         if (x.leader()) out->status = -1;

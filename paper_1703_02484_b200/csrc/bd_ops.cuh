@@ -32,6 +32,8 @@ BD_HD void op_enter(X& x, Ctx& c) {
         c.w.ctl->status = 0;
         c.w.ctl->err_i = 0;
         c.w.ctl->err_k = 0;
+        c.w.ctl->scratch[0] = ~0ull;  // first bad index of check_finite
+        c.w.ctl->scratch[1] = ~0ull;
     }
     x.sync();
 }
