@@ -37,6 +37,10 @@ from paper_1703_02484_b200.roofline import hbm_peak_gbs, phase_roofline, step_by
 
 C0 = [(0.5, 3.0, 3.0), (0.5, -3.0, -1.5)]
 FLOPS_PER_PAIR = 23  # algorithmic FP64 flops per directed pair (_kernels.py:48-56)
+# the symmetric evaluation's own count per directed pair: per unordered pair the
+# shared geometry (min image 12, r^2 3, sqrt + mul 2, reciprocal 1) plus per
+# direction alpha*w and two (mul + add) accumulations (5 x 2) = 28
+SYM_FLOPS_PER_PAIR = 14
 # FP64 instructions the pair kernel's inner loop executes per DIRECTED pair (SASS of the hot loop;
 # DESIGN.md §3.1): fast-sym evaluates each unordered pair once (14.62 per unordered pair in the
 # factored uniform loop: 256 DFMA + 130 DMUL + 82 DADD per 8 sources x 4 receivers), fast is the
@@ -56,6 +60,8 @@ def parse():
                     help="auto = fast-sym (Newton's third law on r^-3; sharded by block pairs + all-reduce)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-steps", type=int, default=2,
+                    help="--impl reference: full steps of the real reference (baseline/_ref, numba) to time too")
     return ap.parse_args()
 
 
@@ -200,6 +206,10 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        dist.barrier()
+        nccl = ".".join(map(str, torch.cuda.nccl.version())) if not gloo_test else None
+        print(f"[bench] rank {rank}/{world} on cuda:{dev_index} ({torch.cuda.get_device_name(dev_index)}), "
+              f"backend {dist.get_backend()}, nccl {nccl}, communicator up", file=sys.stderr, flush=True)
     n = args.n
     if args.precision == "auto":
         args.precision = "fast-sym"
@@ -294,10 +304,11 @@ def run_ours(args):
                "d2h_bytes_per_step": n * 16 + 8 * _abi.STATS_WORDS, "steps": k2,
                "path": "LongRangeSimulation.step() with positions uploaded from / read back to pinned host memory"}
 
+    failed = bool(bad) or not rep.ok
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
-        return
+        return 1 if failed else 0
     fp64 = fp64_peak_tflops()
     pairs = n * (n - 1)
     f_ms = float(np.mean(force_ms))
@@ -327,10 +338,19 @@ def run_ours(args):
     launches_per_step = {"fast-sym": 15, "fast": 10, "exact": 3 if world == 1 else 5}[args.precision]
     inst = FP64_INST_PER_PAIR.get(args.precision)
     hw = 2 * inst * pairs / (f_ms * 1e-3) / 1e12 if inst else None
+    # roofline of the dominant kernel (the all-pairs force): the FP64 pipe.
+    # achieved = the FP64 work the kernel really executes per step (SASS
+    # FP64 instructions per pair x 2 flops per DFMA-slot) over the force
+    # phase's device time; peak = the measured DFMA throughput, so frac is
+    # the FP64-pipe fraction.  The reference's arithmetic (23 flops per
+    # directed pair) and the symmetric algorithm's own count
+    # (14 per directed pair: the geometry of a pair is shared by its two
+    # directions) are reported beside it.
+    sym_flops = {"fast-sym": SYM_FLOPS_PER_PAIR}.get(args.precision, FLOPS_PER_PAIR)
     line = {
         "metric": "particle-steps/s (N x steps / s), long-range all-pairs + Delaunay maintenance + overlap correction",
-        "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "value": None if failed else value, "unit": "particle-steps/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference init_system restatement, seed 0)",
         "config": {"workload": f"cfg3: N={n} long-range all-pairs + periodic Delaunay triangulation, rho={args.rho}, "
                                f"c0 charges, dt=0.01, D=0.01", "n": n, "rho": args.rho,
@@ -340,22 +360,24 @@ def run_ours(args):
                    "l2": "flushed before every timed step (256 MiB write), flush excluded from the device time"},
         "phase_ms": {"force": f_ms, "maintain": float(np.mean(maint_ms))},
         "interactions_per_s": pairs / (f_ms * 1e-3),
-        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
+        "roofline": {"bound": "fp64", "achieved": hw if hw else achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (hw if hw else achieved) / peak, "traffic": traffic,
                      "peak_source": "measured DFMA probe on this GPU (bd_probe_fp64)" if fp64
                      else "nominal 148x64x2x1.965GHz",
-                     "kernel": kname, "flops_per_pair": FLOPS_PER_PAIR,
-                     "fp64_pipe_active_pct_ncu": pipe,
+                     "kernel": kname,
                      "fp64_inst_per_pair": inst,
-                     "hw_achieved": hw, "hw_frac": hw / peak if hw else None,
-                     "note": "compute-bound FP64 kernel; achieved = 23 algorithmic flops per DIRECTED pair "
-                             "(the reference's arithmetic, SURVEY 8(d)) over the device time of the whole force "
-                             "phase (sort, pack, tie check, pair kernel, combine). fast-sym evaluates each "
-                             "unordered pair once, so it needs fewer flops than that count and frac can exceed 1. "
-                             "hw_achieved is the hardware-side figure: the FP64 instructions the kernel executes "
-                             "(fp64_inst_per_pair, SASS) x 2 flops per DFMA slot over the same time; hw_frac is "
-                             "the fraction of the FP64 pipe it keeps busy. traffic = DRAM bytes per launch of "
-                             "the pair kernel from the committed ncu --set full capture (profiles/)"},
+                     "fp64_pipe_active_pct_ncu": pipe,
+                     "algorithmic_tflops": sym_flops * pairs / (f_ms * 1e-3) / 1e12,
+                     "algorithmic_flops_per_directed_pair": sym_flops,
+                     "reference_equiv_tflops": achieved, "reference_flops_per_directed_pair": FLOPS_PER_PAIR,
+                     "note": "achieved = FP64 work executed: SASS FP64 instructions per directed pair of the pair "
+                             "kernel's hot loop (fp64_inst_per_pair) x 2 flops per DFMA slot x N(N-1) over the "
+                             "device time of the whole force phase (sort, tie check, pack, pair kernel, partial "
+                             "sums), so frac = the fraction of the measured FP64 pipe peak the force phase keeps "
+                             "busy. algorithmic_tflops counts the symmetric algorithm's flops (14 per directed "
+                             "pair); reference_equiv_tflops counts the reference's 23 per directed pair (> peak "
+                             "is possible since each unordered pair is evaluated once). traffic = DRAM bytes "
+                             "per launch of the pair kernel (committed ncu --set full capture, profiles/)"},
         "maintain_roofline": {
             "bound": "hbm", "kernel": "k_step_tri_grid (persistent O(N) step)",
             "achieved": float(np.sum(m_bytes) / (np.sum(m_ms) * 1e-3) / 1e9), "unit": "GB/s",
@@ -376,9 +398,12 @@ def run_ours(args):
         "audit_ok": bool(rep.ok),
         "setup_s": t_setup,
     }
+    if failed:
+        line["error"] = f"{len(bad)} timed steps failed (first: {bad[0] if bad else None}); audit ok: {rep.ok}"
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+    return 1 if failed else 0
 
 
 def sys_first_forces(n, pos, alpha, mu, box):
@@ -405,11 +430,19 @@ def profiled_traffic(kernel: str):
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU implementation of the step, as the
-    C oracle port (kind "port"; the reference is Python and cannot travel to
-    the GPU box), on all host threads.  Each step is a bounded sample: the
-    all-pairs force on a receiver slice x all sources scaled to N + one full
-    maintenance step (integrate, flips, overlap correction) on all N."""
+    """--impl reference: the reference's CPU implementation of the step on
+    the host cores, as the C oracle port (kind "port": oracle/bd_oracle.c,
+    the reference step restated in C with its expression order; the
+    reference itself is Python and cannot be compiled into oracle/_ref).
+    Every timed step is a FULL unsampled step from the evolving state: the
+    all-pairs force on all N receivers (OpenMP over all host threads, like
+    numba's prange in _kernels.py:37) + integrate, pass-through check,
+    inversion repair, Lawson flips and overlap correction (serial, like the
+    reference).  The CPU port needs no warm-up (no JIT): at most one untimed
+    warm-up step is run.  When the reference package itself is installed
+    under baseline/_ref, its own LongRangeSimulation (numba
+    + numpy) is timed too for --ref-steps full steps, as a second stated
+    baseline (`reference_numba`)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -425,55 +458,119 @@ def run_reference(args):
     tri = O.OracleTri.from_arrays(arrays, n, box.length)
     tri.restore_delaunay(pos)
     t_build = time.perf_counter() - t0
-    # forces of the initial state (oracle, all threads; untimed setup)
-    forces, _ = O.long_range(pos, alpha, mu, box.length, threads)
-    sim = O.OracleSim(pos, alpha, mu, box.length, tri=tri, force_mode=-1, seed=0, stream=2, threads=threads)
-    fn = _oracle_range_fn()
-    ns = min(n, max(256, int(1.0e9 / n)))
-    out = np.empty((n, 2))
-    err = np.empty(n, np.int64)
-    times, tf, tm = [], [], []
-    for s in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        fn(sim.pos.ctypes.data, sim.alpha.ctypes.data, sim.mu.ctypes.data, n, float(box.length), threads, 0, ns,
-           out.ctypes.data, err.ctypes.data)
-        t_force = (time.perf_counter() - t0) * n / ns
-        sim.force[...] = forces
+    tri0 = {k: v.copy() for k, v in tri.arrays().items()}  # the port's steps mutate `tri` in place
+    sim = O.OracleSim(pos, alpha, mu, box.length, tri=tri, force_mode=0, seed=0, stream=2, threads=threads)
+    warm = min(args.warmup, 1)
+    times = []
+    for s in range(warm + args.steps):
         t0 = time.perf_counter()
         st = sim.step()
-        t_maint = time.perf_counter() - t0
+        dt = time.perf_counter() - t0
         if st["status"] != 0:
-            break
-        if s >= args.warmup:
-            times.append(t_force + t_maint)
-            tf.append(t_force)
-            tm.append(t_maint)
+            raise RuntimeError(f"oracle step {s} failed: {st}")
+        if s >= warm:
+            times.append(dt)
     t_step = float(np.mean(times))
     value = n / t_step
-    sample = (f"per step: oracle C port of the reference step -- all-pairs force on {ns} of {n} receivers x all "
-              f"sources scaled to N (mean {np.mean(tf):.2f} s) + one full maintenance step on all N (mean "
-              f"{np.mean(tm):.3f} s); OpenMP {threads} threads for the force (numba prange in the reference), "
-              f"serial elsewhere (as the reference)")
+    sample = (f"full unsampled steps of cfg3 from the evolving state: oracle C port of the reference step "
+              f"(gcc -O2 -ffp-contract=off), all-pairs force on all {n} receivers with OpenMP over {threads} host "
+              f"threads (numba prange in the reference), the rest serial (as the reference); {args.steps} timed "
+              f"steps after {warm} untimed (no JIT to warm)")
     line = {"impl": "reference", "metric": "particle-steps/s (N x steps / s), long-range all-pairs + Delaunay "
                                            "maintenance + overlap correction",
             "value": value, "unit": "particle-steps/s", "n_gpus": args.gpus, "steps": len(times),
-            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": warm, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
             "config": {"workload": f"cfg3: N={n} long-range all-pairs + periodic Delaunay triangulation, "
                                    f"rho={args.rho}, c0 charges, dt=0.01, D=0.01", "n": n, "rho": args.rho},
             "dtype": "f64", "data": "synthetic (reference init_system restatement, seed 0)",
             "cpu_baseline": {"value": value, "unit": "particle-steps/s", "cores": threads, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": "particle-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "setup_build_s": t_build}
+            "step_s": times, "setup_build_s": t_build}
+    if args.ref_steps > 0:
+        line["reference_numba"] = time_reference_numba(args, box, pos, types, alpha, mu, tri0, threads)
     print(json.dumps(line))
+
+
+def time_reference_numba(args, box, pos, types, alpha, mu, tri0, threads):
+    """The reference package itself (baseline/_ref, pip-installed from the
+    reference's pkg/ with --no-deps) on its stock code path:
+    brownsim.dynamics.LongRangeSimulation.step with its own numpy RngStream
+    (0, 2), numba threads = all host cores.  The initial triangulation is
+    the reference's (build_initial_arrays + restore_delaunay: array for
+    array what brownsim.triangulation.build_initial returns, which takes
+    ~25 s at this N).  Returns a stated baseline object, or why not."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "brownsim")):
+        return {"unavailable": "baseline/_ref/brownsim not installed"}
+    try:
+        sys.path.insert(0, ref)
+        import numba
+        import brownsim
+        from brownsim import _kernels as RK
+        from brownsim.core import ParticleSystem as RPS, PeriodicBox as RBox, RngStream as RRng, SimParams as RSP
+        from brownsim.dynamics import LongRangeSimulation as RLR
+        from brownsim.triangulation import PeriodicTriangulation as RTri
+        numba.set_num_threads(min(threads, numba.config.NUMBA_NUM_THREADS))
+        # JIT warm-up: two steps of a small system compile every kernel the step uses
+        t0 = time.perf_counter()
+        from brownsim.initial import InitConfig as RIC, init_system as rinit
+        from brownsim.core import box_length_for_density as rblen
+        from brownsim.triangulation import build_initial as rbuild
+        wbox = RBox(rblen(256, 1.0, 0.3))
+        wsys = rinit(RIC(n=256, box=wbox, sigma=1.0, types=C0, seed=0))
+        wsim = RLR(wsys, RSP(n=256, sigma=1.0, dt=0.01, diffusion=0.01), RRng(0, stream=2),
+                   tri=rbuild(wsys.positions, wbox))
+        wsim.step()
+        wsim.step()
+        t_jit = time.perf_counter() - t0
+        rbox = RBox(float(box.length))
+        rsys = RPS(pos.copy(), types.copy(), alpha.copy(), mu.copy(), rbox)
+        rtri = RTri(rbox, pos.shape[0], **tri0)
+        rsim = RLR(rsys, RSP(n=pos.shape[0], sigma=1.0, dt=0.01, diffusion=0.01), RRng(0, stream=2), tri=rtri)
+        times, parts = [], []
+        for _ in range(args.ref_steps):
+            t0 = time.perf_counter()
+            st = rsim.step()
+            times.append(time.perf_counter() - t0)
+            parts.append({"force_ms": st.force_ms, "maintain_ms": st.maintain_ms, "overlap_ms": st.overlap_ms})
+        t = float(np.mean(times))
+        return {"value": pos.shape[0] / t, "unit": "particle-steps/s", "cores": int(numba.get_num_threads()),
+                "kind": "reference", "steps": len(times), "step_s": times, "phases": parts, "jit_s": t_jit,
+                "sample": f"brownsim {getattr(brownsim, '__version__', '0.1.0')} LongRangeSimulation.step, "
+                          f"{len(times)} full steps from the initial state after a JIT warm-up (2 steps of a 256-particle system); numba "
+                          f"{numba.__version__} threads = {numba.get_num_threads()} (only the all-pairs kernel "
+                          f"is threaded, the rest is numpy / Python on one core)"}
+    except Exception as exc:  # pragma: no cover
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: start N ranks (one process per GPU)
+    under torch.distributed.run on this node and return its exit code."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.run(cmd).returncode
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:
-        run_ours(args)
+        sys.exit(run_ours(args))
 
 
 if __name__ == "__main__":

@@ -268,6 +268,14 @@ int bd_tri_restore_delaunay(const bd_state_t* s, const bd_params_t* p, int64_t* 
 int bd_integrate(const bd_state_t* s, const bd_params_t* p, double dt, int64_t* crossings,
                  int64_t* result, void* stream);
 
+/* dynamics.integrate (dynamics.py:73-94) with normals drawn by the caller:
+ * noise (n,2) f64 standard normals -- e.g. the reference's own
+ * rng.normals((n, 2)) (core.py:131-133, dynamics.py:89) -- clamped to
+ * +-p->clamp on the device like clamped_normals (core.py:151-154); the call
+ * counter *s->call is not touched.  Otherwise as bd_integrate. */
+int bd_integrate_noise(const bd_state_t* s, const bd_params_t* p, double dt, const double* noise,
+                       int64_t* crossings, int64_t* result, void* stream);
+
 /* PeriodicTriangulation.apply_crossings (triangulation.py:166-177);
  * crossings (n,2) int64 */
 int bd_tri_apply_crossings(const bd_state_t* s, const bd_params_t* p, const int64_t* crossings,

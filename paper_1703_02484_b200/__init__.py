@@ -8,7 +8,7 @@ state read-out; every step runs on the GPU through libbd_b200.so
 
 from .core import (BrownsimError, BuildError, ConfigError, CounterRng, NonConvergenceError, ParticleSystem,
                    PeriodicBox, RngStream, SimParams, SingularityError, StepFailure, box_length_for_density,
-                   min_image_disp, wrap)
+                   clamped_gaussian, clamped_normals, min_image_disp, wrap)
 from .initial import InitConfig, init_arrays, init_system, reservoir_sample, triangular_lattice
 
 __version__ = "0.1.0"

@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(STEP_BT) k_restore_delaunay_grid(bd_state_t s,
 // ---- method-boundary ops (bd_ops.cuh), one cooperative launch each --------
 enum : int64_t {
     OP_INTEGRATE = 1, OP_APPLY_CROSSINGS, OP_EDGE_INVERSION, OP_SIGNED_AREA2, OP_DELAUNAY_FLAGS,
-    OP_INVERTED_FLAGS, OP_FLIP_EDGES, OP_REPAIR, OP_RESTORE, OP_CORRECT_OVERLAPS
+    OP_INVERTED_FLAGS, OP_FLIP_EDGES, OP_REPAIR, OP_RESTORE, OP_CORRECT_OVERLAPS, OP_INTEGRATE_NOISE
 };
 
 struct OpArgs {
@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(STEP_BT) k_op_grid(bd_state_t s, bd_params_t p
         case OP_REPAIR: op_repair_inversions(x, c, a.i0, a.i1 != 0, a.res); break;
         case OP_RESTORE: op_restore_delaunay(x, c, a.i0, a.res); break;
         case OP_CORRECT_OVERLAPS: op_correct_overlaps(x, c, a.i0, a.i1 != 0, a.res); break;
+        case OP_INTEGRATE_NOISE: op_integrate(x, c, a.d0, (int64_t*)a.out, a.res, (const double*)a.in); break;
         default: break;
     }
 }
@@ -1004,6 +1005,13 @@ int bd_tri_restore_delaunay(const bd_state_t* s, const bd_params_t* p, int64_t* 
 int bd_integrate(const bd_state_t* s, const bd_params_t* p, double dt, int64_t* crossings, int64_t* result,
                  void* stream) {
     return launch_op(s, p, OpArgs{OP_INTEGRATE, 0, 0, dt, nullptr, crossings, result}, p->n, (cudaStream_t)stream);
+}
+
+int bd_integrate_noise(const bd_state_t* s, const bd_params_t* p, double dt, const double* noise, int64_t* crossings,
+                       int64_t* result, void* stream) {
+    if (!noise) return -(int)cudaErrorInvalidValue;
+    return launch_op(s, p, OpArgs{OP_INTEGRATE_NOISE, 0, 0, dt, noise, crossings, result}, p->n,
+                     (cudaStream_t)stream);
 }
 
 int bd_tri_apply_crossings(const bd_state_t* s, const bd_params_t* p, const int64_t* crossings, void* stream) {

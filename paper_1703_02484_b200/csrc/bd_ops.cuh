@@ -38,9 +38,11 @@ BD_HD void op_enter(X& x, Ctx& c) {
     x.sync();
 }
 
-// integrate: res = {status, n_crossed, err_i}; crossings (n,2) int64 (may be null)
+// integrate: res = {status, n_crossed, err_i}; crossings (n,2) int64 (may be
+// null); noise (n,2) caller-drawn standard normals (null: the counter noise of
+// call *s.call, which then advances; given: the call counter is left alone)
 template <class X>
-BD_HD void op_integrate(X& x, Ctx& c, double dt, int64_t* crossings, int64_t* res) {
+BD_HD void op_integrate(X& x, Ctx& c, double dt, int64_t* crossings, int64_t* res, const double* noise = nullptr) {
     Red<X> R(x);
     op_enter(x, c);
     bd_stats_t st;
@@ -52,9 +54,9 @@ BD_HD void op_integrate(X& x, Ctx& c, double dt, int64_t* crossings, int64_t* re
         }
         return;
     }
-    const u64 nc = ph_integrate(x, R, c, dt, crossings);
+    const u64 nc = ph_integrate(x, R, c, dt, crossings, noise);
     if (x.leader()) {
-        *c.s.call = c.call + 1;
+        if (!noise) *c.s.call = c.call + 1;
         res[0] = 0;
         res[1] = (int64_t)nc;
         res[2] = 0;

@@ -313,14 +313,20 @@ BD_HD void ph_tri_copy(X& x, const bd_tri_t& a, bd_tri_t& b) {
 
 // integrate (dynamics.py:73-94) fused with the crossing bookkeeping; returns #particles that crossed
 template <class X>
-BD_HD u64 ph_integrate(X& x, Red<X>& R, Ctx& c, double dt, int64_t* cross64 = nullptr) {
+BD_HD u64 ph_integrate(X& x, Red<X>& R, Ctx& c, double dt, int64_t* cross64 = nullptr,
+                       const double* noise = nullptr) {
     c.work[WK_INTEGRATE]++;
     u64* r = R.open();
     const double L = c.p.L, scale = sqrt(c.p.diffusion * dt), clamp = c.p.clamp;
     double* pos = c.s.pos;
     for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
         double z0, z1;
-        normal_pair(c.p.seed, c.p.stream, c.call, (uint64_t)i, 0, z0, z1);
+        if (noise) {  // caller-drawn normals (the reference's own rng.normals((n, 2)))
+            z0 = noise[2 * i];
+            z1 = noise[2 * i + 1];
+        } else {
+            normal_pair(c.p.seed, c.p.stream, c.call, (uint64_t)i, 0, z0, z1);
+        }
         const double z[2] = {clampd(z0, clamp), clampd(z1, clamp)};
         int crossed = 0;
         for (int k = 0; k < 2; ++k) {
@@ -537,12 +543,18 @@ BD_HD int64_t restore_delaunay_full(X& x, Red<X>& R, Ctx& c, int64_t max_passes)
         }
         passes++;
         if (passes > max_passes) {
+            // error exits also retire this call's stamps (a caller may catch
+            // the error and call again: its stamps must not look current)
+            if (x.leader()) c.w.ctl->gen = gen0 + (u64)passes + 1;
             set_error(x, c, BD_ERR_NONCONV, passes, 0);
             x.sync();
             return -1;
         }
         ph_select_and_flip(x, R, c, nullptr, 0, c.w.stamp, (uint32_t)(gen0 + (u64)passes));
-        if (x.ld(&c.w.ctl->status)) return -1;
+        if (x.ld(&c.w.ctl->status)) {
+            if (x.leader()) c.w.ctl->gen = gen0 + (u64)passes + 1;
+            return -1;
+        }
     }
 }
 
@@ -571,12 +583,16 @@ BD_HD int64_t restore_delaunay(X& x, Red<X>& R, Ctx& c, int64_t max_passes) {
         }
         passes++;
         if (passes > max_passes) {
+            if (x.leader()) c.w.ctl->gen = gen0 + (u64)passes + 1;  // retire this call's stamps (see above)
             set_error(x, c, BD_ERR_NONCONV, passes, 0);
             x.sync();
             return -1;
         }
         ph_select_and_flip(x, R, c, flagged, (int64_t)nflag);
-        if (x.ld(&c.w.ctl->status)) return -1;
+        if (x.ld(&c.w.ctl->status)) {
+            if (x.leader()) c.w.ctl->gen = gen0 + (u64)passes + 1;
+            return -1;
+        }
         // candidates of the next pass (deduplicated by a per-call generation stamp)
         const int ring = (int)(passes & 3);
         u64* nc = &lens[4 + ring];

@@ -1,17 +1,24 @@
 """Multi-GPU sharding of the all-pairs force (one process per GPU).
 
-Only the O(N^2) force is partitioned: every rank holds the
-full simulation state, computes the forces of its own contiguous block of
-receiver slots, and the (fx, fy, flag) records of all slots are all-gathered
-over NCCL (NVLink/NVSwitch) into one (n, 3) buffer that every rank scatters
-into its force array.  The O(N) path -- integrate, triangulation
-maintenance, Verlet lists, overlap correction -- then runs as identical,
+Only the O(N^2) force is partitioned; every rank holds the
+full simulation state.  The O(N) path -- integrate, triangulation
+maintenance, Verlet lists, overlap correction -- runs as identical,
 deterministic replicas on every rank, so no further collective is needed
 (its per-pass global barriers would cost more over NVLink than the work;
-DESIGN.md §Multi-GPU).  Each receiver's sum is computed whole by one rank
-in the same order, so results are bit-identical for any world size.
+DESIGN.md §7).  Two decompositions:
 
-Per step the collective moves 24 B x N (3 MiB at N = 131,072).
+  * FAST / EXACT (`force`): each rank computes the forces of its own
+    contiguous block of receiver slots and the (fx, fy, flag) records of all
+    slots are all-gathered (24 B x N per step).  Each receiver's sum is
+    computed whole by one rank in one order, so the forces are
+    bit-identical for every world size.
+  * FAST-SYM (`force_sym`, the default precision): each rank evaluates its
+    share of the unordered block pairs and writes an (n, 2) partial; the
+    partials are summed by an all-reduce (16 B x N).  The result is
+    identical on every rank of one run, but its last bits depend on the
+    world size and on the all-reduce's summation order (NCCL picks ring or
+    tree); against the single-GPU FAST-SYM forces it agrees to ~1e-15
+    relative (tests/test_distributed.py, tests/test_multirank_gpu.py).
 """
 
 from __future__ import annotations

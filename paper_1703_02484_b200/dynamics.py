@@ -35,6 +35,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _abi
+from ._hostview import HostView, Versioned
 from ._lib import check, lib, require_cuda
 from .core import (BrownsimError, CounterRng, NonConvergenceError, ParticleSystem, SimParams, SingularityError,
                    StepFailure)
@@ -142,36 +143,68 @@ class _Engine:
         check(lib().bd_clear_status(ctypes.byref(self.s), _stream()), "bd_clear_status")
 
 
+def _check_rng(rng):
+    """The device draws counter-based noise, so `rng` must be
+    a CounterRng.  The reference's RngStream (numpy Philox + ziggurat,
+    core.py:111-139) is not counter-addressable: name the replacement."""
+    if all(hasattr(rng, k) for k in ("seed", "stream", "call")):
+        return
+    if hasattr(rng, "seed") and hasattr(rng, "stream"):
+        raise BrownsimError(
+            f"rng {type(rng).__name__}(seed={rng.seed}, stream={rng.stream}) draws numpy ziggurat normals, which the "
+            f"device cannot reproduce; pass paper_1703_02484_b200.CounterRng({rng.seed}, {rng.stream}) instead "
+            f"(same key; the reference replays its normals with oracle.noise_np.CounterNormals({rng.seed}, "
+            f"{rng.stream}))")
+    raise BrownsimError("the device noise is counter-based: rng must be a CounterRng(seed, stream[, call])")
+
+
 def _rng_counter(rng):
-    for k in ("seed", "stream", "call"):
-        if not hasattr(rng, k):
-            raise BrownsimError("the device noise is counter-based: rng must be a CounterRng (seed, stream, call)")
+    _check_rng(rng)
     return int(rng.seed) & ((1 << 64) - 1), int(rng.stream) & ((1 << 64) - 1), int(rng.call)
 
 
 def integrate(sys: ParticleSystem, forces, params: SimParams, rng, dt: float | None = None) -> np.ndarray:
     """dynamics.py:73-94 on the GPU: one Euler-Maruyama update of all
     positions (prev <- pos; pos = wrap((pos + F dt) + xi sqrt(D dt)), xi the
-    clamped counter normals of call rng.call, which advances by one);
-    returns the box crossings (N, 2) int64.  Non-finite forces raise
-    StepFailure before anything moves."""
+    +-noise_clamp clamped normals); returns the box crossings (N, 2) int64.
+    Non-finite forces raise StepFailure before anything moves.
+
+    With a CounterRng, xi are the counter normals of call rng.call (drawn
+    on the device; the call advances by one).  Any other rng with the
+    reference's `normals(shape, dtype)` method -- e.g. the reference's own
+    numpy RngStream -- is asked for one (N, 2) block exactly like the
+    reference does (dynamics.py:89), which is uploaded and used instead."""
     import torch
     from ._ops import OpState, as_device
     if dt is None:
         dt = params.dt
-    seed, stream, call = _rng_counter(rng)
     n = sys.n
     f = as_device(forces, torch.float64, sys.device, (n, 2))
     op = OpState(n, sys.box.length, sys.device)
     op.p.diffusion, op.p.clamp, op.p.sigma = float(params.diffusion), float(params.noise_clamp), float(params.sigma)
-    op.p.seed, op.p.stream = seed, stream
-    op.call_t.fill_(call)
     cross = torch.zeros((n, 2), dtype=torch.int64, device=sys.device)
     op.bind(pos=sys.positions_t, prev=sys.positions_prev_t, force=f, image=sys.image_t)
-    res = op.run("bd_integrate", ctypes.c_double(float(dt)), ctypes.c_void_p(cross.data_ptr()), op.res_ptr)
+    counter = all(hasattr(rng, k) for k in ("seed", "stream", "call"))
+    if counter:
+        seed, stream, call = _rng_counter(rng)
+        op.p.seed, op.p.stream = seed, stream
+        op.call_t.fill_(call)
+    else:
+        if not torch.isfinite(f).all():  # the reference checks before it draws (dynamics.py:84-86)
+            bad = int((~torch.isfinite(f).all(dim=1)).nonzero()[0, 0].item())
+            raise StepFailure(f"non-finite force on particle {bad}")
+        xi = as_device(np.ascontiguousarray(rng.normals((n, 2), dtype=np.float64), dtype=np.float64),
+                       torch.float64, sys.device, (n, 2))
+    sys.bump_version()
+    if counter:
+        res = op.run("bd_integrate", ctypes.c_double(float(dt)), ctypes.c_void_p(cross.data_ptr()), op.res_ptr)
+    else:
+        res = op.run("bd_integrate_noise", ctypes.c_double(float(dt)), ctypes.c_void_p(xi.data_ptr()),
+                     ctypes.c_void_p(cross.data_ptr()), op.res_ptr)
     if res[0] == _abi.BD_ERR_STEPFAIL:
         raise StepFailure(f"non-finite force on particle {int(res[2])}")
-    rng.call = call + 1
+    if counter:
+        rng.call = call + 1
     return cross.cpu().numpy()
 
 
@@ -193,6 +226,9 @@ def correct_overlaps(sys: ParticleSystem, pair_a, pair_b, params: SimParams, tri
     op.p.max_overlap_iters = int(params.max_overlap_iters)
     flags = torch.zeros(n, dtype=torch.uint8, device=sys.device)
     op.bind(pos=sys.positions_t, pair_a=pa, pair_b=pb, overlap_flags=flags, image=sys.image_t)
+    sys.bump_version()
+    if tri is not None:
+        tri.bump_version()
     res = op.run("bd_overlap_correct", m, int(tri is not None), op.res_ptr)
     if flags_out is not None:
         flags_out |= flags.cpu().numpy().astype(bool)
@@ -252,6 +288,7 @@ class _SimulationBase:
         self.sys = sys
         self.params = params
         self.rng = rng if rng is not None else CounterRng(0, 2)
+        _check_rng(self.rng)
         self.debug_scan = debug_scan
         self.collect_flags = collect_flags
         self.step_index = 0
@@ -293,6 +330,13 @@ class _SimulationBase:
                 on_step(self, out[-1])
         return out
 
+    def _bump_versions(self):
+        self.sys.bump_version()
+        if getattr(self, "tri", None) is not None:
+            self.tri.bump_version()
+        if getattr(self, "abp", None) is not None:
+            self.abp.bump_version()
+
     def _launch_force(self):
         pass
 
@@ -301,6 +345,7 @@ class _SimulationBase:
 
     def _run_batch(self, steps: int) -> list:
         import torch
+        self._bump_versions()  # host copies read before these steps go stale
         stats = torch.zeros((steps, _abi.STATS_WORDS), dtype=torch.int64, device=self.sys.device)
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps + 1)]
         evs[0].record()
@@ -445,12 +490,13 @@ class ShortRangeSimulation(_SimulationBase):
                                    ctypes.c_void_p(stats_ptr), _stream()), "bd_step_verlet")
 
 
-class AbpState:
+class AbpState(Versioned):
     """Director angles and self-propulsion parameters (dynamics.py:60-66).
 
     Once a simulation owns it, the angles live on the device (`angles_t`);
-    the `angles` attribute reads / writes them as a numpy array, like the
-    reference's in-place numpy array."""
+    the `angles` attribute reads them as a write-through numpy copy
+    (`abp.angles[i] = v` reaches the device, like the reference's in-place
+    numpy array)."""
 
     def __init__(self, angles, speed: float, rot_diffusion: float):
         self.speed = float(speed)
@@ -466,14 +512,17 @@ class AbpState:
 
     @property
     def angles(self) -> np.ndarray:
-        return self.angles_t.cpu().numpy() if self.angles_t is not None else self._host
+        return HostView(self.angles_t, self, "angles") if self.angles_t is not None else self._host
 
     @angles.setter
     def angles(self, value):
         import torch
         v = np.ascontiguousarray(value, dtype=np.float64).reshape(-1)
         if self.angles_t is not None:
+            if v.shape != tuple(self.angles_t.shape):
+                raise BrownsimError(f"angles must have shape {tuple(self.angles_t.shape)}, got {v.shape}")
             self.angles_t.copy_(torch.from_numpy(v))
+            self.bump_version()
         else:
             self._host = v.copy()
 

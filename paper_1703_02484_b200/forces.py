@@ -111,13 +111,66 @@ class VerletList:
         return int(self.pair_a.shape[0])
 
 
-def build_verlet(positions, box: PeriodicBox, r_list: float, skin: float, overlap_margin=None) -> VerletList:
-    """Every unordered pair within r_list, in the reference's exact order
-    (cell scan, forces.py:120-150 / _kernels.py:141-236), built on the GPU."""
+@dataclass
+class CellGrid:
+    """Uniform periodic bins (forces.py:67-78): `order` = particle ids sorted
+    by cell (stable), `cell_start` = CSR bounds.  Device tensors here."""
+
+    cells_per_axis: int
+    cell_edge: float
+    order: object  # torch int64 (N,)
+    cell_start: object  # torch int64 (ncells + 1,)
+
+    @property
+    def n_cells(self) -> int:
+        return self.cells_per_axis * self.cells_per_axis
+
+
+def build_cell_grid(positions, box: PeriodicBox, cell_edge: float):
+    """forces.py:81-99: bin wrapped positions into cells of edge >= cell_edge;
+    None when fewer than 3 cells fit per axis (the caller pairs by brute
+    force).  Computed on the device with the reference's formula (floor,
+    clip, stable sort, bincount, cumsum).  build_verlet does its own binning
+    in the Verlet kernel and only looks at whether the grid is None."""
     torch = require_cuda()
-    pos = positions if hasattr(positions, "data_ptr") else torch.from_numpy(
-        np.ascontiguousarray(positions, dtype=np.float64)).cuda()
-    pos = pos.contiguous()
+    ncx = int(math.floor(box.length / cell_edge))
+    if ncx < 3:
+        return None
+    edge = box.length / ncx
+    pos = _as_positions(positions)
+    ij = torch.floor(pos / edge).to(torch.int64).clamp_(0, ncx - 1)
+    cell_id = ij[:, 0] + ij[:, 1] * ncx
+    order = torch.sort(cell_id, stable=True).indices
+    counts = torch.bincount(cell_id, minlength=ncx * ncx)
+    cell_start = torch.zeros(ncx * ncx + 1, dtype=torch.int64, device=pos.device)
+    torch.cumsum(counts, 0, out=cell_start[1:])
+    return CellGrid(ncx, edge, order, cell_start)
+
+
+def _as_positions(positions):
+    torch = require_cuda()
+    if hasattr(positions, "data_ptr"):
+        return positions.contiguous()
+    return torch.from_numpy(np.ascontiguousarray(positions, dtype=np.float64)).cuda()
+
+
+def build_verlet(*args, **kwargs) -> VerletList:
+    """Every unordered pair within r_list, in the reference's exact order
+    (cell scan, forces.py:120-150 / _kernels.py:141-236), built on the GPU.
+
+    Signature of the reference: build_verlet(grid, positions, box, r_list,
+    skin, overlap_margin=None); build_verlet(positions, box, r_list, skin,
+    overlap_margin=None) is accepted too.  The device kernel bins the
+    particles itself, with the same rule as build_cell_grid (fewer than 3
+    cells per axis -> np.triu_indices order), so `grid` only has to be
+    build_cell_grid's answer for the same positions."""
+    if len(args) >= 2 and isinstance(args[1], PeriodicBox):
+        positions, box, r_list, skin, *rest = args
+    else:
+        _grid, positions, box, r_list, skin, *rest = args
+    overlap_margin = rest[0] if rest else kwargs.get("overlap_margin")
+    torch = require_cuda()
+    pos = _as_positions(positions)
     n = int(pos.shape[0])
     L = float(box.length)
     cap = verlet_pair_capacity(n, L, r_list)
@@ -143,10 +196,13 @@ def build_verlet(positions, box: PeriodicBox, r_list: float, skin: float, overla
 
 
 def verlet_needs_rebuild(vl: VerletList, positions, box: PeriodicBox) -> bool:
-    """forces.py:153-156 on the GPU (max_sq_displacement kernel)."""
+    """forces.py:153-156 on the GPU (max_sq_displacement kernel); positions
+    may be a numpy array or a device tensor."""
     torch = require_cuda()
-    out = torch.zeros(1, dtype=torch.float64, device=vl.snapshot.device)
-    check(lib().bd_max_sq_displacement(positions.data_ptr(), vl.snapshot.data_ptr(), int(positions.shape[0]),
+    pos = _as_positions(positions)
+    snap = _as_positions(vl.snapshot)
+    out = torch.zeros(1, dtype=torch.float64, device=snap.device)
+    check(lib().bd_max_sq_displacement(pos.data_ptr(), snap.data_ptr(), int(pos.shape[0]),
                                        float(box.length), out.data_ptr(), _stream()), "bd_max_sq_displacement")
     return bool(out.item() > (vl.skin / 2.0) ** 2)
 

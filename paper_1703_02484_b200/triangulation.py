@@ -22,6 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from ._hostview import HostView, Versioned
 from .core import BrownsimError, BuildError, NonConvergenceError, PeriodicBox
 
 DEFAULT_TOL = 1e-12
@@ -73,7 +74,7 @@ class AuditReport:
                 and self.n_incircle_violations == 0)
 
 
-class PeriodicTriangulation:
+class PeriodicTriangulation(Versioned):
     """Vertex/edge/triangle arrays with opposite-vertex links on the torus."""
 
     def __init__(self, box: PeriodicBox, n_vertices: int, tri_v, tri_shift, tri_edge, edge_v, edge_tri,
@@ -104,10 +105,11 @@ class PeriodicTriangulation:
     def backup_tensors(self) -> dict:
         return self._backup
 
-    # host copies (numpy), named like the reference's attributes
+    # host copies (numpy, write-through: _hostview.HostView), named like the
+    # reference's attributes; `tri.edge_tri[e, 0] = x` reaches the device
     def __getattr__(self, name):
         if name in TRI_KEYS:
-            return self._t[name].cpu().numpy()
+            return HostView(self._t[name], self, name)
         raise AttributeError(name)
 
     def arrays(self) -> dict:
@@ -117,6 +119,7 @@ class PeriodicTriangulation:
         import torch
         for k in TRI_KEYS:
             self._t[k].copy_(torch.from_numpy(np.ascontiguousarray(arrays[k], dtype=_DTYPES[k])))
+        self.bump_version()
 
     @property
     def n_triangles(self) -> int:
@@ -136,6 +139,7 @@ class PeriodicTriangulation:
     def restore_state(self, state):
         for k in TRI_KEYS:
             self._t[k].copy_(state[k])
+        self.bump_version()
 
     # -- device methods (the reference's method boundary, csrc/bd_ops.cuh) --
     # Each runs one cooperative launch on this triangulation's device arrays
@@ -144,6 +148,7 @@ class PeriodicTriangulation:
 
     def _ops(self, n_pairs: int = 0):
         from ._ops import OpState
+        self.bump_version()  # the op may rewrite the arrays: older host copies go stale
         return OpState(self.n_vertices, self.box.length, self.device, tri=self, n_pairs=n_pairs, tol=self.tol)
 
     def _pos(self, positions):

@@ -5,7 +5,7 @@ tests/golden/make_golden_msd.py from the reference with the counter noise).
   oracle  -> final positions bit-exact after 1,000 steps
   gpu EXACT -> final positions bit-exact after 1,000 steps; MSD(t) from the
           device image counters equal to the reference's MSD to 1e-9
-  gpu FAST  -> MSD(t) within 3 standard deviations of the reference's
+  gpu FAST, FAST-SYM -> MSD(t) within 3 standard deviations of the reference's
           run-to-run spread at every checkpoint (FAST sums the all-pairs force
           in another order, |dF|/|F| ~ 1e-13; the trajectories then drift
           apart, the statistics must not).  The spread is measured on the
@@ -63,9 +63,38 @@ def test_gpu_exact_1000_steps_bitwise_and_msd():
 
 
 @pytest.mark.gpu
-def test_gpu_fast_msd_statistics():
-    sim, msd = run_gpu("fast")
+@pytest.mark.parametrize("precision", ["fast", "fast-sym"])
+def test_gpu_fast_msd_statistics(precision):
+    sim, msd = run_gpu(precision)
     runs = np.vstack([G["msd"][None], G["msd_other_seeds"]])
     sd = runs.std(axis=0, ddof=1)
     assert (np.abs(msd - G["msd"]) <= 3.0 * sd).all(), (msd, G["msd"], sd)
     assert sim.tri.audit(sim.sys.positions).ok
+
+
+@pytest.mark.gpu
+def test_gpu_fast_sym_force_free_diffusion_slope():
+    """The reference's criterion 6 (tests/test_acceptance.py:196-219) through
+    the whole FAST-SYM step: with zero charges and a dilute system the MSD
+    grows as 2 * m2 * D * t, m2 = 0.99499 the second moment of the +-3
+    clamped normal (free diffusion; overlap corrections are rare at
+    rho = 0.02).  65,536 particles x 100 steps: the statistical error of the
+    slope is ~0.4 %, the tolerance 2 %."""
+    from paper_1703_02484_b200.core import (CounterRng, ParticleSystem, PeriodicBox, SimParams,
+                                            box_length_for_density)
+    from paper_1703_02484_b200.dynamics import LongRangeSimulation
+    from paper_1703_02484_b200.initial import InitConfig, init_arrays
+    n, D, dt, steps = 65536, 0.01, 0.01, 100
+    box = PeriodicBox(box_length_for_density(n, 1.0, 0.02))
+    pos, t, _, _ = init_arrays(InitConfig(n=n, box=box, sigma=1.0, types=[(1.0, 0.0, 0.0)], seed=3))
+    z = np.zeros(n)
+    sys_ = ParticleSystem(pos, t, z, z, box)
+    sim = LongRangeSimulation(sys_, SimParams(n=n, sigma=1.0, dt=dt, diffusion=D), CounterRng(5, 2),
+                              precision="fast-sym")
+    u0 = sys_.unwrapped_positions().clone()
+    sim.run(steps)
+    d = sys_.unwrapped_positions() - u0
+    msd = float((d * d).sum(1).mean().item())
+    m2 = 0.99499
+    slope = msd / (steps * dt)
+    assert abs(slope - 2 * m2 * D) <= 0.02 * 2 * m2 * D, (slope, 2 * m2 * D)
