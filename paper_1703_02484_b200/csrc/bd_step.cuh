@@ -240,9 +240,21 @@ BD_HD bool crossed_side(const bd_tri_t& T, const double* pos, const double* prv,
 }
 
 // flip_edge + _relink, triangulation.py:254-302 (conflict-free flips may run concurrently)
+// An outer edge of one selected quad can be an outer edge of another one
+// flipped concurrently: each flip rewrites only the side that referenced
+// its own old triangle, but finding that side reads the other side's word,
+// which the other flip may be writing.  The side is therefore claimed with
+// a compare-and-swap on side 0 (the other flip's triangles never equal
+// ours, so the outcome does not depend on the interleaving, and no plain
+// read races a plain write: compute-sanitizer racecheck clean).
 BD_HD void relink(bd_tri_t& T, int64_t edge, int32_t old_tri, int32_t new_tri, int8_t opp) {
+#if defined(__CUDA_ARCH__)
+    const int side = atomicCAS(&T.edge_tri[2 * edge], old_tri, new_tri) == old_tri ? 0 : 1;
+    if (side) T.edge_tri[2 * edge + 1] = new_tri;
+#else
     const int side = T.edge_tri[2 * edge] == old_tri ? 0 : 1;
     T.edge_tri[2 * edge + side] = new_tri;
+#endif
     T.edge_opp[2 * edge + side] = opp;
 }
 

@@ -33,8 +33,8 @@ SUITES = {
     "test_forces.py": {"long_range_kernel", "short_range_kernel", "cell_pairs", "max_sq_displacement"},
     "test_triangulation.py": {"tri.restore_delaunay", "tri.repair_inversions", "tri.flip_edge",
                               "tri.apply_crossings", "tri.delaunay_flags"},
-    "test_dynamics.py": {"integrate", "correct_overlaps", "overlap_pass_kernel", "long_range_kernel",
-                         "tri.edge_inversion_present"},
+    "test_dynamics.py": {"integrate", "correct_overlaps", "long_range_kernel", "short_range_kernel",
+                         "tri.edge_inversion_present", "tri.repair_inversions", "tri.restore_delaunay"},
     "test_acceptance.py": {"long_range_kernel", "integrate", "correct_overlaps", "tri.restore_delaunay"},
 }
 

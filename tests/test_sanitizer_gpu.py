@@ -9,7 +9,8 @@ path adds race and memory checking).
   memcheck  -- out-of-bounds / misaligned accesses in every step kernel,
                the grid driver and the method-boundary ops
   synccheck -- illegal barrier usage (divergent __syncthreads / grid syncs)
-Each run must end with "ERROR SUMMARY: 0 errors" and the workload's own
+Each run must report no hazard / error (racecheck: "0 hazards displayed
+(0 errors, 0 warnings)", the others: "ERROR SUMMARY: 0 errors") and the workload's own
 parity check must still pass (tools/sanitize_run.py prints OK)."""
 
 import os
@@ -38,5 +39,7 @@ def test_compute_sanitizer_clean(tool, what, env):
     cmd += [sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py"), what]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, env={**os.environ, **env})
     out = r.stdout + r.stderr
-    assert "ERROR SUMMARY: 0 errors" in out and r.returncode == 0, out[-4000:]
+    clean = "RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)" if tool == "racecheck" \
+        else "ERROR SUMMARY: 0 errors"
+    assert clean in out and r.returncode == 0, out[-4000:]
     assert f"OK {what}" in out, out[-4000:]
