@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=131072)
+    ap.add_argument("--particles", "--n", dest="n", type=int, default=131072)
     ap.add_argument("--rho", type=float, default=0.3)
     ap.add_argument("--precision", default="auto", choices=["auto", "fast-sym", "fast", "exact"],
                     help="auto = fast-sym (Newton's third law on r^-3; sharded by block pairs + all-reduce)")
@@ -553,8 +553,12 @@ def relaunch(args):
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
+    # the script's own options go after the script path; spell them out in full so that
+    # torch.distributed.run's parser cannot take one for an abbreviation of its own (--n)
+    own = ["--particles" if a == "--n" else ("--particles=" + a[4:] if a.startswith("--n=") else a)
+           for a in sys.argv[1:]]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + own
     print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
     return subprocess.run(cmd).returncode
 

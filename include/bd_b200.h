@@ -213,6 +213,16 @@ int bd_force_sym_partial(const bd_state_t* s, const bd_params_t* p, int rank, in
                          void* stream);
 int bd_force_sym_finish(const bd_state_t* s, const bd_params_t* p, const double* part, void* stream);
 
+/* the FAST-SYM work split of rank `rank` of `world` (host only, no device
+ * call): out[11] = {block slots B, blocks Mb, circulant half-range D,
+ * chunks S, distances per chunk, chunks [c0, c1), source-side distances
+ * [d0, d1), diagonal blocks [i0, i1)}.  Rank r owns every unordered block
+ * pair (I, I + d mod Mb) with d in [d0, d1) (for even Mb, d = D only for
+ * I < Mb / 2) and the diagonal blocks I in [i0, i1); together the ranks
+ * cover every unordered pair of slots exactly once (the multi-GPU split of
+ * the prange over receivers, _kernels.py:37). */
+int bd_sym_shard(int64_t n, int rank, int world, int64_t* out);
+
 /* the rest of LongRangeSimulation.step after the force (dynamics.py:196-274):
  * integrate, pass-through check, inversion repair, Delaunay restoration,
  * overlap correction with the joint fixed point, rollback -- one persistent

@@ -54,6 +54,15 @@ def shard_for(n: int, rank: int, world: int) -> Shard:
     return Shard(rank, world, (chunk + SLOT_ALIGN - 1) // SLOT_ALIGN * SLOT_ALIGN)
 
 
+def sym_shard(n: int, rank: int, world: int) -> dict:
+    """The FAST-SYM work split of one rank (bd_sym_shard; host-only, no GPU
+    needed): which unordered block pairs and diagonal blocks it evaluates."""
+    out = (ctypes.c_int64 * 11)()
+    check(lib().bd_sym_shard(int(n), int(rank), int(world), out), "bd_sym_shard")
+    keys = ("block", "blocks", "D", "chunks", "per", "c0", "c1", "d0", "d1", "i0", "i1")
+    return dict(zip(keys, (int(v) for v in out)))
+
+
 class ShardedLongRange:
     """Receiver-slot sharding of the all-pairs force over a process group.
 
