@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(BLOCK_BT) k_step_tri_block(bd_state_t s, bd_pa
 // ~600 from L2.  ~184 bytes per particle: N <= ~1200 within the 227 KB opt-in.
 struct SmemState {
     int64_t tri_v, tri_shift, tri_edge, edge_v, edge_tri, edge_opp, pos, prev;
-    int64_t inc_off, inc_cur, inc, eovl, estat, cross8, tinv, total;
+    int64_t inc_off, inc_cur, inc, eovl, estat, ewin, cross8, tinv, total;
 };
 
 BD_HD int64_t al16(int64_t x) { return (x + 15) & ~(int64_t)15; }
@@ -113,6 +113,7 @@ BD_HD SmemState smem_state(int64_t n, int64_t ne, int64_t nt) {
     l.inc = o; o = al16(o + 8 * ne);
     l.eovl = o; o = al16(o + ne);
     l.estat = o; o = al16(o + ne);
+    l.ewin = o; o = al16(o + 4 * ne);
     l.cross8 = o; o = al16(o + 2 * n);
     l.tinv = o; o = al16(o + nt);
     l.total = o;
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(BLOCK_BT) k_step_tri_block_smem(bd_state_t s, 
     blk_copy(ls.tri.edge_opp, s.tri.edge_opp, 2 * ne);
     blk_copy(ls.pos, s.pos, 16 * n);
     blk_copy(ls.prev, s.prev, 16 * n);
+    for (int64_t i = threadIdx.x; i < ne; i += blockDim.x) ((uint32_t*)(sm + l.ewin))[i] = 0u;
     __syncthreads();
     Ctx c = make_ctx(ls, p);
     c.w.inc_off = (int32_t*)(sm + l.inc_off);  // scratch: rebuilt / rewritten before every use
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(BLOCK_BT) k_step_tri_block_smem(bd_state_t s, 
     c.w.inc = (int32_t*)(sm + l.inc);
     c.w.eovl = (uint8_t*)(sm + l.eovl);
     c.w.estat = (uint8_t*)(sm + l.estat);
+    c.w.ewin = (uint32_t*)(sm + l.ewin);  // stamps: zeroed below (a stale shared-memory value could look current)
     c.w.cross8 = (int8_t*)(sm + l.cross8);
     c.w.tinv = (uint8_t*)(sm + l.tinv);
     ExecBlock x{c.w.ctl};

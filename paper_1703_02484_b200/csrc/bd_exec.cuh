@@ -35,6 +35,7 @@ struct Ctl {
     u64 lists[8];   // worklist lengths (restore_delaunay): two rings of 4
     u64 gen;        // worklist dedup generation
     u64 vgen;       // correct_overlaps: generation of the per-particle overlap stamps
+    u64 wgen;       // ph_select_and_flip: last LFMIS round stamp
     u64 bsum[4096]; // per-block partial sums (grid scans)
 };
 

@@ -34,6 +34,7 @@ struct Ws {
     int32_t* wl0;      // (ne) restore_delaunay worklist: flagged edges
     int32_t* wl1;      // (ne) restore_delaunay worklist: edges to re-evaluate
     uint32_t* stamp;   // (ne) worklist dedup stamps
+    uint32_t* ewin;    // (ne) LFMIS: round stamp of the selection of each edge (ph_select_and_flip)
     uint32_t* vhit;    // (n) correct_overlaps: sweep stamp of the particles with an overlapping pair
     double* src4;      // all-pairs scratch (packed sources / sorted FAST workspace)
     // Verlet list (forces.py:67-156)
@@ -56,7 +57,7 @@ BD_HD int64_t ncells_of(const bd_params_t& p) { return p.ncx > 0 ? p.ncx * p.ncx
 
 // layout of bd_workspace_bytes(); offsets relative to the workspace base
 struct WsLayout {
-    int64_t ctl, contrib, estat, eovl, tinv, cross8, image_bk, inc_off, inc_cur, inc, wl0, wl1, stamp, vhit, src4;
+    int64_t ctl, contrib, estat, eovl, tinv, cross8, image_bk, inc_off, inc_cur, inc, wl0, wl1, stamp, ewin, vhit, src4;
     int64_t cell_id, cell_start, cell_cur, corder, pcnt, vinc_off, vinc_cur, vinc, ov_idx, sr_err, sr_force, total;
 };
 
@@ -78,6 +79,7 @@ BD_HD WsLayout ws_layout(const bd_params_t& p, int64_t ne, int64_t nt) {
     l.wl0 = o; o = align_up(o + 4 * ne);
     l.wl1 = o; o = align_up(o + 4 * ne);
     l.stamp = o; o = align_up(o + 4 * ne);
+    l.ewin = o; o = align_up(o + 4 * ne);
     l.vhit = o; o = align_up(o + 4 * n);
     // all-pairs scratch: packed double4 sources (EXACT) or the sorted FAST workspace
     {
@@ -117,6 +119,7 @@ BD_HD Ws ws_carve(void* base, const bd_params_t& p, int64_t ne, int64_t nt) {
     w.wl0 = (int32_t*)(b + l.wl0);
     w.wl1 = (int32_t*)(b + l.wl1);
     w.stamp = (uint32_t*)(b + l.stamp);
+    w.ewin = (uint32_t*)(b + l.ewin);
     w.vhit = (uint32_t*)(b + l.vhit);
     w.src4 = (double*)(b + l.src4);
     w.cell_id = (int32_t*)(b + l.cell_id);
@@ -423,10 +426,19 @@ BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c, const int32_t* list = null
                              uint32_t* dirty = nullptr, uint32_t gen = 0) {
     bd_tri_t& T = c.s.tri;
     uint8_t* st = c.w.estat;
+    uint32_t* ewin = c.w.ewin;
     const int64_t cnt = list ? m : T.ne;
     u64 nsel_total = 0;
-    for (;;) {
+    // Round r marks its winners with stamp s0 + r in ewin (never read in the
+    // phase that writes it); the states in st change only in the second
+    // phase, where every thread writes its own edges and reads only ewin.
+    // No read races a write: compute-sanitizer racecheck clean.  Stamps of
+    // earlier calls are < s0 (a monotone counter in the control block).
+    const uint32_t s0 = (uint32_t)x.ld(&c.w.ctl->wgen) + 1;
+    uint32_t stamp = s0;
+    for (;; ++stamp) {
         c.work[WK_LFMIS_ROUND]++;
+        // an undecided edge wins when no lower-id edge of its two triangles is undecided or selected
         u64* rs = R.open();
         for (int64_t j = x.tid(); j < cnt; j += x.nth()) {
             const int64_t e = list ? list[j] : j;
@@ -445,20 +457,25 @@ BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c, const int32_t* list = null
                     }
                 }
             }
-            if (win) st[e] = ES_SEL;
+            if (win) ewin[e] = stamp;
             R.add((u64)win);
         }
         nsel_total += R.close(rs);
+        // winners -> selected; an undecided edge next to an edge selected in this call -> removed
         u64* ru = R.open();
         for (int64_t j = x.tid(); j < cnt; j += x.nth()) {
             const int64_t e = list ? list[j] : j;
             if (st[e] != ES_UND) continue;
+            if (ewin[e] == stamp) {
+                st[e] = ES_SEL;
+                continue;
+            }
             bool blocked = false;
             for (int side = 0; side < 2 && !blocked; ++side) {
                 const int64_t t = T.edge_tri[2 * e + side];
                 for (int k = 0; k < 3; ++k) {
                     const int64_t f = T.tri_edge[3 * t + k];
-                    if (f != e && st[f] == ES_SEL) {
+                    if (f != e && ewin[f] >= s0 && ewin[f] <= stamp) {
                         blocked = true;
                         break;
                     }
@@ -469,6 +486,7 @@ BD_HD u64 ph_select_and_flip(X& x, Red<X>& R, Ctx& c, const int32_t* list = null
         }
         if (R.close(ru) == 0) break;
     }
+    if (x.leader()) c.w.ctl->wgen = stamp;  // read again only after the flip phase's barrier
     if (nsel_total == 0) return 0;
     c.work[WK_FLIPS] += (int64_t)nsel_total;
     for (int64_t j = x.tid(); j < cnt; j += x.nth()) {
