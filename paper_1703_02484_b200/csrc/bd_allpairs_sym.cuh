@@ -587,10 +587,6 @@ BD_DEV bool near_window(uint64_t b0, uint64_t b1, uint64_t T, double eps) {
 BD_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 constexpr int SY_NW2 = SY_CT / 32;   // warps per CTA
-// BD_SY_SYNC 1: a CTA barrier ends every tile; 0: decoupled warps (tickets)
-#ifndef BD_SY_SYNC
-#define BD_SY_SYNC 1
-#endif
 constexpr int SY_NS = 2;             // source stages
 // dynamic smem per stage: positions (16 B) + alphas (8 B) of SY_TS sources,
 // the warps' source-side sums (16 B per source and warp); + the lanes' receiver sums
@@ -618,19 +614,17 @@ BD_DEV void sym_issue(const SymWs& w, int64_t n, int64_t t, unsigned char* smem,
 // instead of forming a tail.  Warp v of block I owns slots
 // I*SY_BT + 32 SY_R v + lane + 32 m, m < SY_R.  Its receiver sums over the
 // chunk go to apart[c]; the CTA's source-side sums of each tile of block
-// J = I + d go to bpart[d - 1].
-// The warps run decoupled (no CTA barrier in the tile loop): a warp that
-// finishes a tile takes a ticket on the stage; the last of the SY_NW2 warps
-// adds the warps' source-side sums of the tile (in warp order) into bpart
-// and refills the stage with the tile two ahead.  A warp whose tiles are
-// more expensive (per-pair image modes) delays the others by at most a
-// stage instead of at every tile.
+// J = I + d go to bpart[d - 1].  A CTA barrier ends every tile; the stage
+// is then refilled (TMA) with the tile two ahead while the CTA adds its
+// warps' source-side sums.  (Measured and dropped: decoupled warps with a
+// per-stage ticket, the last warp summing and refilling -- 10.2 vs 9.5 ms at
+// cfg3; persistent CTAs over an atomic work counter -- 9.7 vs 9.4 ms: the
+// hot loop's code generation got worse.)
 __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int64_t n, double L, double lo, double hi,
                                                                      int chunk0, int64_t i0, int64_t i1) {
     extern __shared__ __align__(128) unsigned char sy_smem[];
     double* accs = reinterpret_cast<double*>(sy_smem + SY_NS * SY_STAGE);  // [SY_R][2][SY_CT]
     __shared__ __align__(8) uint64_t bars[SY_NS];
-    __shared__ int tickets[SY_NS];
     __shared__ uint64_t wband[SY_NW2][2][4];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t Mb = sym_blocks(n), D = sym_D(n);
@@ -723,10 +717,7 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
     const int64_t nq = d1 > d0 ? (d1 - d0) * tpb : 0;
 
     if (threadIdx.x == 0) {
-        for (int k = 0; k < SY_NS; ++k) {
-            mbar_init(&bars[k], 1);
-            tickets[k] = 0;
-        }
+        for (int k = 0; k < SY_NS; ++k) mbar_init(&bars[k], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -816,7 +807,6 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
                 }
             }
         }
-#if BD_SY_SYNC
         __syncthreads();  // stage st consumed; the warps' source-side sums of tile qi complete
         if (threadIdx.x == 0 && qi + SY_NS < nq) {
             fence_proxy_async_smem();
@@ -832,35 +822,6 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
                 w.bpart[(size_t)(d - 1) * n * 2 + (size_t)base * 2 + e] = v;
             }
         }
-#else
-        // this warp is done with tile qi: ticket; the last warp sums the warps and refills the stage
-        __threadfence_block();
-        __syncwarp();
-        int tk = 0;
-        if (lane == 0) tk = atomicAdd(&tickets[st], 1);
-        tk = __shfl_sync(0xffffffffu, tk, 0);
-        if (tk == SY_NW2 - 1) {
-            __threadfence_block();
-            if (use && d > 0) {
-                // CTA sum of the warp sums (warp order) -> one partial per (d, source)
-                for (int e = lane; e < 2 * cnt; e += 32) {
-                    double v = 0.0;
-#pragma unroll
-                    for (int ww = 0; ww < SY_NW2; ++ww) v += bw[(size_t)ww * SY_TS * 2 + e];
-                    w.bpart[(size_t)(d - 1) * n * 2 + (size_t)base * 2 + e] = v;
-                }
-            }
-            __syncwarp();
-            if (lane == 0) {
-                tickets[st] = 0;
-                if (qi + SY_NS < nq) {
-                    fence_proxy_async_smem();
-                    sym_issue(w, n, ((I + d0 + (qi + SY_NS) / tpb) % Mb) * tpb + (qi + SY_NS) % tpb, sy_smem, bars,
-                              st);
-                }
-            }
-        }
-#endif
     }
 #pragma unroll
     for (int m = 0; m < SY_R; ++m) {
