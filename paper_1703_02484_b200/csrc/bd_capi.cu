@@ -56,7 +56,7 @@ int64_t block_max_n() {
     static int64_t v = -1;
     if (v < 0) {
         const char* e = getenv("BD_BLOCK_MAX_N");
-        v = e ? atoll(e) : 4096;
+        v = e ? atoll(e) : 1536;
     }
     return v;
 }
@@ -1110,6 +1110,34 @@ int bd_probe_fp64(int64_t iters, double* out, void* stream, double* flops_out) {
     k_probe_fp64<<<nb, 256, 0, (cudaStream_t)stream>>>(iters, out);
     *flops_out = 2.0 * 8.0 * (double)iters * (double)nb * 256.0;
     return err_code(cudaGetLastError());
+}
+
+// ---- grid-barrier probe (measurement only): latency of the cooperative
+// grid.sync the step drivers end every phase with (tools/probe_barrier.py)
+__global__ void k_probe_gridsync(int64_t iters, int mode, unsigned* bar) {
+    for (int64_t i = 0; i < iters; ++i) cooperative_groups::this_grid().sync();
+}
+
+int bd_probe_barrier(int64_t iters, int mode, int ctas_per_sm, int threads, void* scratch, void* stream,
+                     double* ms_out) {
+    init_device_info();
+    unsigned* bar = (unsigned*)scratch;  // [0, 256): barrier words + error count; from byte 256: a Ctl block
+    cudaMemsetAsync(bar, 0, 256, (cudaStream_t)stream);
+    void* args[] = {&iters, &mode, &bar};
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, (cudaStream_t)stream);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_probe_gridsync, dim3(g_num_sms * ctas_per_sm),
+                                                dim3(threads), args, 0, (cudaStream_t)stream);
+    cudaEventRecord(e1, (cudaStream_t)stream);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *ms_out = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return err_code(e);
 }
 
 const char* bd_build_info(void) {

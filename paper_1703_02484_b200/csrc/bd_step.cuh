@@ -183,6 +183,9 @@ BD_HD void ctx_init_work(Ctx& c) {
 // device wall clock (ns) for the phase breakdown; 0 on the host emulation
 BD_HD int64_t now_ns() {
 #if defined(__CUDA_ARCH__)
+    // only the leader's timers are reported (bd_stats_t.work); the other
+    // threads skip the (slow) global-timer read
+    if (threadIdx.x != 0 || blockIdx.x != 0) return 0;
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return (int64_t)t;
@@ -306,24 +309,33 @@ BD_HD int flip_edge(bd_tri_t& T, int64_t e) {
 // ---------------------------------------------------------------------------
 // phases
 
+// dst[0, bytes) = src[0, bytes) by the policy's threads (no barrier)
+template <class X>
+BD_HD void copy_bytes(X& x, void* dst, const void* src, int64_t bytes) {
+    unsigned char* d = (unsigned char*)dst;
+    const unsigned char* s = (const unsigned char*)src;
+    int64_t body = 0;
+    if ((((uintptr_t)d | (uintptr_t)s) & 15) == 0) {
+        body = bytes & ~(int64_t)15;
+        struct alignas(16) V16 {
+            unsigned long long a, b;
+        };
+        for (int64_t i = x.tid(); i < body / 16; i += x.nth()) ((V16*)d)[i] = ((const V16*)s)[i];
+    }
+    for (int64_t i = body + x.tid(); i < bytes; i += x.nth()) d[i] = s[i];
+}
+
 // copy the six triangulation arrays a -> b (save_state / restore_state)
 template <class X>
 BD_HD void ph_tri_copy(X& x, const bd_tri_t& a, bd_tri_t& b) {
-    for (int64_t t = x.tid(); t < a.nt; t += x.nth()) {
-        for (int k = 0; k < 3; ++k) {
-            b.tri_v[3 * t + k] = a.tri_v[3 * t + k];
-            b.tri_edge[3 * t + k] = a.tri_edge[3 * t + k];
-        }
-        for (int k = 0; k < 6; ++k) b.tri_shift[6 * t + k] = a.tri_shift[6 * t + k];
-    }
-    for (int64_t e = x.tid(); e < a.ne; e += x.nth()) {
-        b.edge_v[2 * e] = a.edge_v[2 * e];
-        b.edge_v[2 * e + 1] = a.edge_v[2 * e + 1];
-        b.edge_tri[2 * e] = a.edge_tri[2 * e];
-        b.edge_tri[2 * e + 1] = a.edge_tri[2 * e + 1];
-        b.edge_opp[2 * e] = a.edge_opp[2 * e];
-        b.edge_opp[2 * e + 1] = a.edge_opp[2 * e + 1];
-    }
+    // each array as a flat byte range, 16 bytes per thread and step where
+    // both ends are 16-byte aligned (the device and shared-memory arrays are)
+    copy_bytes(x, b.tri_v, a.tri_v, 12 * a.nt);
+    copy_bytes(x, b.tri_edge, a.tri_edge, 12 * a.nt);
+    copy_bytes(x, b.tri_shift, a.tri_shift, 6 * a.nt);
+    copy_bytes(x, b.edge_v, a.edge_v, 8 * a.ne);
+    copy_bytes(x, b.edge_tri, a.edge_tri, 8 * a.ne);
+    copy_bytes(x, b.edge_opp, a.edge_opp, 2 * a.ne);
 }
 
 // integrate (dynamics.py:73-94) fused with the crossing bookkeeping; returns #particles that crossed
