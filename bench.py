@@ -45,7 +45,8 @@ SYM_FLOPS_PER_PAIR = 14
 # DESIGN.md §3.1): fast-sym evaluates each unordered pair once (14.62 per unordered pair in the
 # factored uniform loop: 256 DFMA + 130 DMUL + 82 DADD per 8 sources x 4 receivers), fast is the
 # directed kernel; each instruction takes one DFMA slot of the FP64 pipe (2 flops at the measured peak)
-FP64_INST_PER_PAIR = {"fast-sym": 14.62 / 2, "fast": 12.0}
+FP64_INST_PER_PAIR = {"fast-sym": 14.875 / 2, "fast": 12.0}  # fallbacks; the ncu capture's count wins
+PROFILE_ROUND = "r02"
 
 
 def parse():
@@ -245,6 +246,10 @@ def run_ours(args):
     K = args.steps
     stats_t = torch.zeros((K, _abi.STATS_WORDS), dtype=torch.int64, device="cuda")
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    from paper_1703_02484_b200._lib import lib as _native
+    timed_kernel = args.precision == "fast-sym"
+    if timed_kernel:
+        _native().bd_timing_enable(K)  # events around each launch of the pair kernel (the dominant kernel)
     if world > 1:
         dist.barrier()
     with ClockSampler(dev_index) as clk:
@@ -259,6 +264,13 @@ def run_ours(args):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    pair_ms = None
+    if timed_kernel:
+        import ctypes
+        buf = (ctypes.c_float * K)()
+        got = _native().bd_timing_read(buf, K)
+        _native().bd_timing_enable(0)
+        pair_ms = [float(buf[i]) for i in range(got)]
     force_ms = [ev[j][0].elapsed_time(ev[j][1]) for j in range(K)]
     maint_ms = [ev[j][1].elapsed_time(ev[j][2]) for j in range(K)]
     ms = float(sum(force_ms) + sum(maint_ms))
@@ -331,21 +343,23 @@ def run_ours(args):
             cpu = {"value": None, "unit": "particle-steps/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {exc}"}
     kname = {"fast-sym": "k_allpairs_sym", "fast": "k_allpairs_fast", "exact": "k_allpairs"}[args.precision]
-    traffic, pipe = profiled_traffic(kname)
+    traffic, pipe, inst_prof = profiled_kernel(kname, n)
     # kernels of ours per step: sort (4) + pack + tie check (4) + pair kernel + partial sums + finish +
     # unsort + rescan (fast-sym); sort (4) + pack + pair kernel + partition sums + unsort + rescan (fast); pack + pair
     # kernel (+ slot copy in / out when sharded) (exact); then the persistent step kernel
     launches_per_step = {"fast-sym": 15, "fast": 10, "exact": 3 if world == 1 else 5}[args.precision]
-    inst = FP64_INST_PER_PAIR.get(args.precision)
-    hw = 2 * inst * pairs / (f_ms * 1e-3) / 1e12 if inst else None
-    # roofline of the dominant kernel (the all-pairs force): the FP64 pipe.
-    # achieved = the FP64 work the kernel really executes per step (SASS
-    # FP64 instructions per pair x 2 flops per DFMA-slot) over the force
-    # phase's device time; peak = the measured DFMA throughput, so frac is
-    # the FP64-pipe fraction.  The reference's arithmetic (23 flops per
-    # directed pair) and the symmetric algorithm's own count
-    # (14 per directed pair: the geometry of a pair is shared by its two
-    # directions) are reported beside it.
+    inst = inst_prof or FP64_INST_PER_PAIR.get(args.precision)
+    # roofline of the dominant kernel (the all-pairs pair kernel): the FP64 pipe.
+    # achieved = the FP64 work the pair kernel executes per launch (FP64
+    # instructions per directed pair, counted by ncu on the same kernel, x 2
+    # flops per DFMA slot x N(N-1)) over its average launch time, measured
+    # live with CUDA events around each launch (bd_timing_*); peak = the
+    # measured DFMA throughput, so frac is the FP64-pipe fraction.  The same
+    # over the whole force phase (sort, pack, tie check, partials) and the
+    # algorithm's own / the reference's flop counts are reported beside it.
+    k_ms = float(np.mean(pair_ms)) if pair_ms else f_ms
+    hw = 2 * inst * pairs / (k_ms * 1e-3) / 1e12 if inst else None
+    hw_phase = 2 * inst * pairs / (f_ms * 1e-3) / 1e12 if inst else None
     sym_flops = {"fast-sym": SYM_FLOPS_PER_PAIR}.get(args.precision, FLOPS_PER_PAIR)
     line = {
         "metric": "particle-steps/s (N x steps / s), long-range all-pairs + Delaunay maintenance + overlap correction",
@@ -365,19 +379,27 @@ def run_ours(args):
                      "peak_source": "measured DFMA probe on this GPU (bd_probe_fp64)" if fp64
                      else "nominal 148x64x2x1.965GHz",
                      "kernel": kname,
+                     "kernel_ms": k_ms, "kernel_ms_source": "CUDA events around each pair-kernel launch "
+                                                             "(bd_timing_enable/read)" if pair_ms else
+                     "force phase events (no per-kernel timing for this precision)",
                      "fp64_inst_per_pair": inst,
+                     "fp64_inst_source": "ncu sm__sass_thread_inst_executed_op_d{fma,mul,add} of the pair kernel "
+                                         f"(profiles/{PROFILE_ROUND}_ncu_full_{kname}.json) / (N(N-1))"
+                     if inst_prof else "SASS count of the hot loop (fallback)",
                      "fp64_pipe_active_pct_ncu": pipe,
-                     "algorithmic_tflops": sym_flops * pairs / (f_ms * 1e-3) / 1e12,
+                     "force_phase_ms": f_ms, "force_phase_achieved": hw_phase,
+                     "force_phase_frac": hw_phase / peak if hw_phase else None,
+                     "algorithmic_tflops": sym_flops * pairs / (k_ms * 1e-3) / 1e12,
                      "algorithmic_flops_per_directed_pair": sym_flops,
-                     "reference_equiv_tflops": achieved, "reference_flops_per_directed_pair": FLOPS_PER_PAIR,
-                     "note": "achieved = FP64 work executed: SASS FP64 instructions per directed pair of the pair "
-                             "kernel's hot loop (fp64_inst_per_pair) x 2 flops per DFMA slot x N(N-1) over the "
-                             "device time of the whole force phase (sort, tie check, pack, pair kernel, partial "
-                             "sums), so frac = the fraction of the measured FP64 pipe peak the force phase keeps "
-                             "busy. algorithmic_tflops counts the symmetric algorithm's flops (14 per directed "
-                             "pair); reference_equiv_tflops counts the reference's 23 per directed pair (> peak "
-                             "is possible since each unordered pair is evaluated once). traffic = DRAM bytes "
-                             "per launch of the pair kernel (committed ncu --set full capture, profiles/)"},
+                     "reference_equiv_tflops": FLOPS_PER_PAIR * pairs / (k_ms * 1e-3) / 1e12,
+                     "reference_flops_per_directed_pair": FLOPS_PER_PAIR,
+                     "note": "achieved = FP64 work the pair kernel executes (fp64_inst_per_pair x 2 flops per "
+                             "DFMA slot x N(N-1)) over its average launch time (kernel_ms, live CUDA events); "
+                             "frac = fraction of the measured FP64 pipe peak. force_phase_* = the same over the "
+                             "whole force phase. algorithmic_tflops counts the symmetric algorithm's flops (14 "
+                             "per directed pair); reference_equiv_tflops the reference's 23 per directed pair "
+                             "(> peak is possible: each unordered pair is evaluated once). traffic = DRAM bytes "
+                             "per launch of the pair kernel (ncu --set full capture, profiles/)"},
         "maintain_roofline": {
             "bound": "hbm", "kernel": "k_step_tri_grid (persistent O(N) step)",
             "achieved": float(np.sum(m_bytes) / (np.sum(m_ms) * 1e-3) / 1e9), "unit": "GB/s",
@@ -414,19 +436,30 @@ def sys_first_forces(n, pos, alpha, mu, box):
     return out
 
 
-def profiled_traffic(kernel: str):
-    """(dram bytes per launch, fp64 pipe %) of `kernel` from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", f"r01_ncu_full_{kernel}.json")
+def profiled_kernel(kernel: str, n: int):
+    """(DRAM bytes per launch, FP64 pipe %, FP64 instructions per directed
+    pair) of `kernel` from this round's committed ncu capture (profiles/;
+    made at the same N by tools/profile.sh), or Nones."""
+    path = os.path.join(ROOT, "profiles", f"{PROFILE_ROUND}_ncu_full_{kernel}.json")
     try:
         for d in json.load(open(path)):
-            if kernel in d["kernel"]:
-                def mb(v):
-                    num, unit = v.split()
-                    return float(num) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
-                return mb(d["dram_read"]) + mb(d["dram_write"]), float(d["fp64_pipe_pct"].split()[0])
+            if kernel not in d["kernel"]:
+                continue
+
+            def num(v):
+                x, unit = (v.split() + [""])[:2]
+                return float(x) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1.0)
+
+            traffic = num(d["dram_read"]) + num(d["dram_write"])
+            pipe = float(d["fp64_pipe_pct"].split()[0])
+            inst = None
+            if "dfma_thread_inst" in d and int(d.get("n", 0)) == n:
+                inst = (num(d["dfma_thread_inst"]) + num(d["dmul_thread_inst"]) + num(d["dadd_thread_inst"])) / (
+                    n * (n - 1.0))
+            return traffic, pipe, inst
     except Exception:
-        return None, None
-    return None, None
+        pass
+    return None, None, None
 
 
 def run_reference(args):

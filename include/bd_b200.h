@@ -352,6 +352,14 @@ int bd_tri_build_initial(const double* pos, int64_t n, double L, const bd_tri_t*
                          int64_t* result, void* stream);
 
 /* library version / build info (host) */
+/* measurement: record CUDA events around the next `launches` launches of
+ * the all-pairs pair kernel (k_allpairs_sym), on the stream they are
+ * launched on; bd_timing_read waits for them and writes each launch's device
+ * time (ms) to ms[0..), returning how many.  bench.py's roofline of the
+ * dominant kernel uses it.  Not thread-safe; off by default. */
+int bd_timing_enable(int64_t launches);
+int64_t bd_timing_read(float* ms, int64_t max_n);
+
 const char* bd_build_info(void);
 
 #ifdef __cplusplus

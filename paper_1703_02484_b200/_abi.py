@@ -106,6 +106,8 @@ def _protos():
         "bd_integrate": ([P(BdState), P(BdParams), c_d, c_vp, c_vp, c_vp], c_int),
         "bd_integrate_noise": ([P(BdState), P(BdParams), c_d, c_vp, c_vp, c_vp, c_vp], c_int),
         "bd_sym_shard": ([c_i64, c_int, c_int, c_vp], c_int),
+        "bd_timing_enable": ([c_i64], c_int),
+        "bd_timing_read": ([c_vp, c_i64], c_i64),
         "bd_tri_apply_crossings": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
         "bd_tri_edge_inversion": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
         "bd_tri_signed_area2": ([P(BdState), P(BdParams), c_vp, c_vp], c_int),
@@ -143,4 +145,4 @@ EXPORTS = ("bd_brute_overlaps", "bd_force","bd_force_prepare", "bd_force_slots",
            "bd_tri_restore_delaunay_ex", "bd_overlap_correct", "bd_tri_copy", "bd_step_abp", "bd_run_abp",
            "bd_tri_build_workspace_bytes", "bd_tri_build_initial",
            "bd_long_range_workspace_bytes_for", "bd_force_sym_partial", "bd_force_sym_finish",
-           "bd_integrate_noise", "bd_sym_shard")
+           "bd_integrate_noise", "bd_sym_shard", "bd_timing_enable", "bd_timing_read")

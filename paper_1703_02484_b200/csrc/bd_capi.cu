@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <mutex>
+#include <vector>
 
 #include "bd_allpairs.cuh"
 #include "bd_allpairs_sym.cuh"
@@ -591,6 +592,23 @@ int launch_fast_finish(const double* pos, int64_t n, const bd_params_t& p, const
 
 // FAST-SYM stage 1 (every rank): sort + pack; pair kernel over this rank's
 // chunks; its partial P_r = A_r - B_r per slot into `part`
+// ---- kernel timing ring (measurement): CUDA events recorded around each
+// launch of the all-pairs pair kernel while enabled (bd_timing_enable), on the
+// launching stream; bench.py reads the per-launch device times back for the
+// roofline of the dominant kernel
+struct TimingRing {
+    std::vector<cudaEvent_t> ev;
+    int64_t next = 0, cap = 0;
+};
+TimingRing g_tr;
+
+void timing_begin(cudaStream_t st) {
+    if (g_tr.cap && g_tr.next < g_tr.cap) cudaEventRecord(g_tr.ev[2 * g_tr.next], st);
+}
+void timing_end(cudaStream_t st) {
+    if (g_tr.cap && g_tr.next < g_tr.cap) cudaEventRecord(g_tr.ev[2 * g_tr.next++ + 1], st);
+}
+
 int launch_sym_partial(const double* pos, const double* alpha, const double* mu, int64_t n, const bd_params_t& p,
                        const SymWs& w, int rank, int world, double* part, cudaStream_t st) {
     init_device_info();
@@ -622,8 +640,10 @@ int launch_sym_partial(const double* pos, const double* alpha, const double* mu,
     k_tie_check<<<grid_for(n), 256, 0, st>>>(n, p.L, w);
     const SymRange g = sym_range(n, rank, world);
     if (g.c1 > g.c0 || g.i1 > g.i0)
+        timing_begin(st);
         k_allpairs_sym<<<dim3((unsigned)sym_blocks(n), (unsigned)(1 + g.c1 - g.c0)), SY_CT, SY_SMEM, st>>>(
             w, n, p.L, p.mi_lo, p.mi_hi, g.c0, g.i0, g.i1);
+        timing_end(st);
     k_sym_partial<<<grid_for(n), 256, 0, st>>>(n, w, g, part);
     return err_code(cudaGetLastError());
 }
@@ -1138,6 +1158,24 @@ int bd_probe_barrier(int64_t iters, int mode, int ctas_per_sm, int threads, void
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return err_code(e);
+}
+
+int bd_timing_enable(int64_t launches) {
+    for (cudaEvent_t e : g_tr.ev) cudaEventDestroy(e);
+    g_tr.ev.assign(2 * (size_t)(launches > 0 ? launches : 0), nullptr);
+    for (auto& e : g_tr.ev) cudaEventCreate(&e);
+    g_tr.cap = launches > 0 ? launches : 0;
+    g_tr.next = 0;
+    return 0;
+}
+
+int64_t bd_timing_read(float* ms, int64_t max_n) {
+    int64_t k = 0;
+    for (; k < g_tr.next && k < max_n; ++k) {
+        cudaEventSynchronize(g_tr.ev[2 * k + 1]);
+        cudaEventElapsedTime(&ms[k], g_tr.ev[2 * k], g_tr.ev[2 * k + 1]);
+    }
+    return k;
 }
 
 const char* bd_build_info(void) {

@@ -77,4 +77,8 @@ def launches(path):
 
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
-    print(json.dumps(raw(path) if mode == "rep" else launches(path), indent=1))
+    res = raw(path) if mode == "rep" else launches(path)
+    if mode == "rep" and len(sys.argv) > 3:  # the problem size the capture ran at (for per-pair counts)
+        for d in res:
+            d["n"] = int(sys.argv[3])
+    print(json.dumps(res, indent=1))

@@ -14,6 +14,7 @@ for what in $P; do
         -o gpurun_out/prof_allpairs_fast python tools/prof_force.py 131072 fast 2 > gpurun_out/ncu_ap.log 2>&1 ;;
     sym)       # FAST-SYM pair kernel (N = 131,072; the bench default)
       timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:k_allpairs_sym -s 1 -c 1 \
+        --metrics sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum \
         -o gpurun_out/prof_allpairs_sym python tools/prof_force.py 131072 fast-sym 2 > gpurun_out/ncu_aps.log 2>&1 ;;
     exact)     # EXACT all-pairs kernel (N = 131,072)
       timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k k_allpairs -c 1 \
