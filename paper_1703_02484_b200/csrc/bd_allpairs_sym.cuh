@@ -81,7 +81,7 @@ constexpr int SY_TS = BD_SY_TS;  // sources per shared-memory stage
 // box): smaller boxes straddle fewer receiver breakpoints, so less of the work
 // runs the per-pair image modes
 #ifndef BD_SY_SUB
-#define BD_SY_SUB 64
+#define BD_SY_SUB 256
 #endif
 constexpr int SY_SUB = BD_SY_SUB;
 static_assert(SY_TS % SY_SUB == 0 && SY_SUB % 32 == 0, "sub-tiles of whole warps");
