@@ -528,20 +528,26 @@ BD_DEV void sym_pass(const SymWs& w, const int64_t* slot, const bool* act, doubl
     }
 }
 
+// the exact min-image modes: one pass per receiver (M0 = 0 .. SY_R - 1)
+template <int MODE, bool FACT, int M0>
+BD_DEV void sym_pass_each(const SymWs& w, const int64_t* slot, const bool* act, double shx, double shy,
+                          const SymStage& sm, int cnt, double L, double lo, double hi, double* bws, int lane,
+                          double ta, double wa, const LaneAcc& acc) {
+    sym_pass<MODE, FACT, M0, 1, M0 == 0>(w, slot, act, shx, shy, sm, cnt, L, lo, hi, bws, lane, ta, wa, acc);
+    if constexpr (M0 + 1 < SY_R)
+        sym_pass_each<MODE, FACT, M0 + 1>(w, slot, act, shx, shy, sm, cnt, L, lo, hi, bws, lane, ta, wa, acc);
+}
+
 // a tile in mode MODE: one pass over all SY_R receivers, except the exact
 // min-image modes (two copies per receiver and axis: passes of one receiver)
 template <int MODE, bool FACT>
 BD_DEV void sym_tile(const SymWs& w, const int64_t* slot, const bool* act, double shx, double shy,
                      const SymStage& sm, int cnt, double L, double lo, double hi, double* bws, int lane, double ta,
                      double wa, const LaneAcc& acc) {
-    static_assert(SY_R == 4, "pass split written for 4 receivers per lane");
     if (MODE < SY_EDGE_M) {
-        sym_pass<MODE, FACT, 0, 4, true>(w, slot, act, shx, shy, sm, cnt, L, lo, hi, bws, lane, ta, wa, acc);
+        sym_pass<MODE, FACT, 0, SY_R, true>(w, slot, act, shx, shy, sm, cnt, L, lo, hi, bws, lane, ta, wa, acc);
     } else {
-        sym_pass<MODE, FACT, 0, 1, true>(w, slot, act, shx, shy, sm, cnt, L, lo, hi, bws, lane, ta, wa, acc);
-        sym_pass<MODE, FACT, 1, 1, false>(w, slot, act, shx, shy, sm, cnt, L, lo, hi, bws, lane, ta, wa, acc);
-        sym_pass<MODE, FACT, 2, 1, false>(w, slot, act, shx, shy, sm, cnt, L, lo, hi, bws, lane, ta, wa, acc);
-        sym_pass<MODE, FACT, 3, 1, false>(w, slot, act, shx, shy, sm, cnt, L, lo, hi, bws, lane, ta, wa, acc);
+        sym_pass_each<MODE, FACT, 0>(w, slot, act, shx, shy, sm, cnt, L, lo, hi, bws, lane, ta, wa, acc);
     }
 }
 
@@ -587,11 +593,19 @@ BD_DEV bool near_window(uint64_t b0, uint64_t b1, uint64_t T, double eps) {
 BD_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 constexpr int SY_NW2 = SY_CT / 32;   // warps per CTA
-constexpr int SY_NS = 2;             // source stages
+#ifndef BD_SY_NS
+#define BD_SY_NS 2
+#endif
+constexpr int SY_NS = BD_SY_NS;      // source stages
 // dynamic smem per stage: positions (16 B) + alphas (8 B) of SY_TS sources,
 // the warps' source-side sums (16 B per source and warp); + the lanes' receiver sums
-constexpr int SY_STAGE = SY_TS * 24 + SY_NW2 * SY_TS * 16;
-constexpr int SY_SMEM = SY_NS * SY_STAGE + SY_R * 2 * SY_CT * 8;
+#ifndef BD_SY_NBW
+#define BD_SY_NBW 1
+#endif
+constexpr int SY_NBW = BD_SY_NBW;  // warp-sum buffers: one per stage, or one shared (+ a barrier per tile)
+constexpr int SY_STAGE = SY_TS * 24;
+constexpr int SY_BWS = SY_NW2 * SY_TS * 16;
+constexpr int SY_SMEM = SY_NS * SY_STAGE + SY_NBW * SY_BWS + SY_R * 2 * SY_CT * 8;
 
 // TMA of source tile t (SY_TS slots; fewer or none past n) into stage st
 BD_DEV void sym_issue(const SymWs& w, int64_t n, int64_t t, unsigned char* smem, uint64_t* bars, int st) {
@@ -623,7 +637,7 @@ BD_DEV void sym_issue(const SymWs& w, int64_t n, int64_t t, unsigned char* smem,
 __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int64_t n, double L, double lo, double hi,
                                                                      int chunk0, int64_t i0, int64_t i1) {
     extern __shared__ __align__(128) unsigned char sy_smem[];
-    double* accs = reinterpret_cast<double*>(sy_smem + SY_NS * SY_STAGE);  // [SY_R][2][SY_CT]
+    double* accs = reinterpret_cast<double*>(sy_smem + SY_NS * SY_STAGE + SY_NBW * SY_BWS);  // [SY_R][2][SY_CT]
     __shared__ __align__(8) uint64_t bars[SY_NS];
     __shared__ uint64_t wband[SY_NW2][2][4];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -736,7 +750,7 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
         const bool use = !(even && d == D && d > 0 && I >= Mb / 2) && cnt > 0;
         unsigned char* stg = sy_smem + (size_t)st * SY_STAGE;
         const SymStage sm{reinterpret_cast<const SymXY*>(stg), reinterpret_cast<const double*>(stg + SY_TS * 16)};
-        double* bw = reinterpret_cast<double*>(stg + SY_TS * 24);  // [SY_NW2][SY_TS][2]
+        double* bw = reinterpret_cast<double*>(sy_smem + SY_NS * SY_STAGE + (st % SY_NBW) * SY_BWS);  // [NW2][TS][2]
         double* bws = bw + (size_t)wid * SY_TS * 2;
         mbar_wait(&bars[st], (uint32_t)((qi / SY_NS) & 1));
         if (use && d == 0) {
@@ -822,6 +836,7 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
                 w.bpart[(size_t)(d - 1) * n * 2 + (size_t)base * 2 + e] = v;
             }
         }
+        if (SY_NBW == 1) __syncthreads();  // the shared warp-sum buffer is written again by the next tile
     }
 #pragma unroll
     for (int m = 0; m < SY_R; ++m) {
