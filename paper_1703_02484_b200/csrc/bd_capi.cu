@@ -80,10 +80,32 @@ __global__ void __launch_bounds__(STEP_BT, MINB) k_step_tri_grid(bd_state_t s, b
     step_tri_after_force(x, c, out);
 }
 
+// One-CTA drivers keep the control block's head (reduction ring, status,
+// generation counters: everything before the grid-scan partials, which
+// ExecBlock never uses) in shared memory for the launch: every phase ends in
+// a reduction whose result all threads read right after the barrier, ~30
+// cycles there instead of an L2 round trip.  Copied in at entry, out at exit.
+constexpr int CTL_HEAD_WORDS = (int)(offsetof(Ctl, bsum) / sizeof(u64));
+
+__device__ Ctl* ctl_in_smem(Ctl* g, u64* sm) {
+    for (int k = threadIdx.x; k < CTL_HEAD_WORDS; k += blockDim.x) sm[k] = ((const u64*)g)[k];
+    __syncthreads();
+    return (Ctl*)sm;
+}
+
+__device__ void ctl_out_smem(Ctl* g, const u64* sm) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < CTL_HEAD_WORDS; k += blockDim.x) ((u64*)g)[k] = sm[k];
+}
+
 __global__ void __launch_bounds__(BLOCK_BT) k_step_tri_block(bd_state_t s, bd_params_t p, bd_stats_t* out) {
     Ctx c = make_ctx(s, p);
+    __shared__ u64 ctl_sm[CTL_HEAD_WORDS];
+    Ctl* const ctl_g = c.w.ctl;
+    c.w.ctl = ctl_in_smem(ctl_g, ctl_sm);
     ExecBlock x{c.w.ctl};
     step_tri_after_force(x, c, out);
+    ctl_out_smem(ctl_g, ctl_sm);
 }
 
 // Small systems: the single-CTA driver keeps the triangulation, the
@@ -122,9 +144,13 @@ BD_HD SmemState smem_state(int64_t n, int64_t ne, int64_t nt) {
 }
 
 __device__ void blk_copy(void* dst, const void* src, int64_t bytes) {
-    const int64_t w = bytes >> 2;
-    for (int64_t i = threadIdx.x; i < w; i += blockDim.x) ((uint32_t*)dst)[i] = ((const uint32_t*)src)[i];
-    for (int64_t i = 4 * w + threadIdx.x; i < bytes; i += blockDim.x) ((uint8_t*)dst)[i] = ((const uint8_t*)src)[i];
+    int64_t done = 0;
+    if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {  // 16 bytes per thread and step
+        const int64_t v = bytes >> 4;
+        for (int64_t i = threadIdx.x; i < v; i += blockDim.x) ((uint4*)dst)[i] = ((const uint4*)src)[i];
+        done = v << 4;
+    }
+    for (int64_t i = done + threadIdx.x; i < bytes; i += blockDim.x) ((uint8_t*)dst)[i] = ((const uint8_t*)src)[i];
 }
 
 __global__ void __launch_bounds__(BLOCK_BT) k_step_tri_block_smem(bd_state_t s, bd_params_t p, bd_stats_t* out) {
@@ -159,8 +185,12 @@ __global__ void __launch_bounds__(BLOCK_BT) k_step_tri_block_smem(bd_state_t s, 
     c.w.ewin = (uint32_t*)(sm + l.ewin);  // stamps: zeroed below (a stale shared-memory value could look current)
     c.w.cross8 = (int8_t*)(sm + l.cross8);
     c.w.tinv = (uint8_t*)(sm + l.tinv);
+    __shared__ u64 ctl_sm[CTL_HEAD_WORDS];
+    Ctl* const ctl_g = c.w.ctl;
+    c.w.ctl = ctl_in_smem(ctl_g, ctl_sm);
     ExecBlock x{c.w.ctl};
     step_tri_after_force(x, c, out);
+    ctl_out_smem(ctl_g, ctl_sm);
     __syncthreads();
     blk_copy(s.tri.tri_v, ls.tri.tri_v, 12 * nt);
     blk_copy(s.tri.tri_shift, ls.tri.tri_shift, 6 * nt);
@@ -181,8 +211,12 @@ __global__ void __launch_bounds__(STEP_BT, MINB) k_step_verlet_grid(bd_state_t s
 
 __global__ void __launch_bounds__(BLOCK_BT) k_step_verlet_block(bd_state_t s, bd_params_t p, bd_stats_t* out) {
     Ctx c = make_ctx(s, p);
+    __shared__ u64 ctl_sm[CTL_HEAD_WORDS];
+    Ctl* const ctl_g = c.w.ctl;
+    c.w.ctl = ctl_in_smem(ctl_g, ctl_sm);
     ExecBlock x{c.w.ctl};
     step_verlet(x, c, out);
+    ctl_out_smem(ctl_g, ctl_sm);
 }
 
 template <int MINB>
@@ -194,8 +228,12 @@ __global__ void __launch_bounds__(STEP_BT, MINB) k_step_abp_grid(bd_state_t s, b
 
 __global__ void __launch_bounds__(BLOCK_BT) k_step_abp_block(bd_state_t s, bd_params_t p, bd_stats_t* out) {
     Ctx c = make_ctx(s, p);
+    __shared__ u64 ctl_sm[CTL_HEAD_WORDS];
+    Ctl* const ctl_g = c.w.ctl;
+    c.w.ctl = ctl_in_smem(ctl_g, ctl_sm);
     ExecBlock x{c.w.ctl};
     step_abp(x, c, out);
+    ctl_out_smem(ctl_g, ctl_sm);
 }
 
 template <class X>
