@@ -73,6 +73,13 @@ BD_DEV Ctx make_ctx(const bd_state_t& s, const bd_params_t& p) {
 }
 
 // ---- persistent drivers: cooperative grid (barrier = grid.sync) and one CTA
+// the triangulation step as one 1024-thread CTA per SM (big_min_n)
+__global__ void __launch_bounds__(1024, 1) k_step_tri_grid_big(bd_state_t s, bd_params_t p, bd_stats_t* out) {
+    Ctx c = make_ctx(s, p);
+    ExecGrid x{c.w.ctl};
+    step_tri_after_force(x, c, out);
+}
+
 template <int MINB>
 __global__ void __launch_bounds__(STEP_BT, MINB) k_step_tri_grid(bd_state_t s, bd_params_t p, bd_stats_t* out) {
     Ctx c = make_ctx(s, p);
@@ -725,12 +732,28 @@ int launch_force(const bd_state_t* s, const bd_params_t* p, cudaStream_t st) {
                      s->force_err, st);
 }
 
+// From this many particles the triangulation step runs as one 1024-thread CTA
+// per SM (k_step_tri_grid_big) instead of 4 x 256: the same threads, a
+// quarter of the barrier arrivals (grid.sync 1.27 vs 1.63 us): cfg3 O(N)
+// step 0.69 -> 0.63 ms.  BD_BIG_MIN_N overrides (0: off).
+int64_t big_min_n() {
+    static int64_t v = -1;
+    if (v < 0) {
+        const char* e = getenv("BD_BIG_MIN_N");
+        v = e ? atoll(e) : 100000;
+    }
+    return v;
+}
+
 int launch_driver(const void* grid_fn, const void* wide_fn, const void* block_fn, const bd_state_t* s,
                   const bd_params_t* p, bd_stats_t* out, cudaStream_t st) {
     init_device_info();
     bd_state_t sv = *s;
     bd_params_t pv = *p;
     void* args[] = {&sv, &pv, &out};
+    if (big_min_n() > 0 && p->n >= big_min_n() && wide_fn == (const void*)k_step_tri_grid<WIDE_MINB>)
+        return err_code(cudaLaunchCooperativeKernel((const void*)k_step_tri_grid_big, dim3(g_num_sms), dim3(1024),
+                                                    args, 0, st));
     if (p->n <= block_max_n())
         return err_code(cudaLaunchKernel(block_fn, dim3(1), dim3(BLOCK_BT), args, 0, st));
     int64_t items = s->tri.ne > p->n ? s->tri.ne : p->n;
