@@ -215,12 +215,13 @@ int bd_force_sym_finish(const bd_state_t* s, const bd_params_t* p, const double*
 
 /* the FAST-SYM work split of rank `rank` of `world` (host only, no device
  * call): out[11] = {block slots B, blocks Mb, circulant half-range D,
- * chunks S, distances per chunk, chunks [c0, c1), source-side distances
- * [d0, d1), diagonal blocks [i0, i1)}.  Rank r owns every unordered block
- * pair (I, I + d mod Mb) with d in [d0, d1) (for even Mb, d = D only for
- * I < Mb / 2) and the diagonal blocks I in [i0, i1); together the ranks
- * cover every unordered pair of slots exactly once (the multi-GPU split of
- * the prange over receivers, _kernels.py:37). */
+ * chunks S, distances per chunk `per`, first chunk c0, chunk stride cs,
+ * chunk count nch, 0, diagonal blocks [i0, i1)}.  Rank r owns the chunks
+ * c = c0 + k cs (k < nch; dealt round-robin), i.e. every unordered block
+ * pair (I, I + d mod Mb) with d in [1 + c per, 1 + (c + 1) per) (capped at
+ * D; for even Mb, d = D only for I < Mb / 2), and the diagonal blocks I in
+ * [i0, i1); together the ranks cover every unordered pair of slots exactly
+ * once (the multi-GPU split of the prange over receivers, _kernels.py:37). */
 int bd_sym_shard(int64_t n, int rank, int world, int64_t* out);
 
 /* the rest of LongRangeSimulation.step after the force (dynamics.py:196-274):

@@ -101,9 +101,8 @@ BD_HD int64_t sym_per(int64_t n) { return (sym_D(n) + sym_chunks(n) - 1) / sym_c
 
 // chunk and distance ranges of rank r of G (see the header comment)
 struct SymRange {
-    int c0, c1;      // chunks [c0, c1)
-    int64_t d0, d1;  // source-side distances [d0, d1), d >= 1
-    int64_t i0, i1;  // diagonal blocks [i0, i1)
+    int c0, cs, nch;  // chunks c0, c0 + cs, c0 + 2 cs, ... (nch of them; interleaved over the ranks)
+    int64_t i0, i1;   // diagonal blocks [i0, i1)
 };
 
 BD_HD SymRange sym_range(int64_t n, int rank, int world);
@@ -623,7 +622,7 @@ BD_DEV void sym_issue(const SymWs& w, int64_t n, int64_t t, unsigned char* smem,
 
 // grid (Mb, 1 + chunks), SY_CT threads.  CTA (x, y): receiver block I = x;
 // y = 0: the diagonal block J = I (directed, receiver side only) when
-// I is in [i0, i1), else nothing; y >= 1: distance chunk c = chunk0 + y - 1.
+// I is in [i0, i1), else nothing; y >= 1: distance chunk c = chunk0 + (y - 1) cstep.
 // The diagonal row comes first so its short CTAs interleave with the rest
 // instead of forming a tail.  Warp v of block I owns slots
 // I*SY_BT + 32 SY_R v + lane + 32 m, m < SY_R.  Its receiver sums over the
@@ -635,7 +634,7 @@ BD_DEV void sym_issue(const SymWs& w, int64_t n, int64_t t, unsigned char* smem,
 // cfg3; persistent CTAs over an atomic work counter -- 9.7 vs 9.4 ms: the
 // hot loop's code generation got worse.)
 __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int64_t n, double L, double lo, double hi,
-                                                                     int chunk0, int64_t i0, int64_t i1) {
+                                                                     int chunk0, int cstep, int64_t i0, int64_t i1) {
     extern __shared__ __align__(128) unsigned char sy_smem[];
     double* accs = reinterpret_cast<double*>(sy_smem + SY_NS * SY_STAGE + SY_NBW * SY_BWS);  // [SY_R][2][SY_CT]
     __shared__ __align__(8) uint64_t bars[SY_NS];
@@ -645,7 +644,7 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
     const int64_t I = blockIdx.x;
     const bool diag = blockIdx.y == 0;
     if (diag && (I < i0 || I >= i1)) return;
-    const int chunk = diag ? SY_S : chunk0 + (int)blockIdx.y - 1;
+    const int chunk = diag ? SY_S : chunk0 + ((int)blockIdx.y - 1) * cstep;
     const LaneAcc acc{accs + threadIdx.x};
 
     int64_t slot[SY_R];
@@ -848,15 +847,15 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
 
 // P = A - B per slot over this rank's chunks / distances / diagonal blocks, fixed order -> part (n, 2)
 __global__ void k_sym_partial(int64_t n, SymWs w, SymRange g, double* __restrict__ part) {
-    const int64_t Mb = sym_blocks(n), D = sym_D(n);
+    const int64_t Mb = sym_blocks(n), D = sym_D(n), per = sym_per(n);
     const bool even = (Mb & 1) == 0;
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
-        // 16-byte loads, 8 in flight (the sums keep their sequential order)
+        // 16-byte loads, the sums in a fixed order: this rank's chunks ascending, the
+        // diagonal block, then the source-side distances of those chunks ascending
         double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
         const double2* ap = reinterpret_cast<const double2*>(w.apart) + s;
-#pragma unroll 8
-        for (int c = g.c0; c < g.c1; ++c) {
-            const double2 v = __ldcs(ap + (size_t)c * n);
+        for (int k = 0; k < g.nch; ++k) {
+            const double2 v = __ldcs(ap + (size_t)(g.c0 + k * g.cs) * n);
             ax += v.x;
             ay += v.y;
         }
@@ -867,13 +866,18 @@ __global__ void k_sym_partial(int64_t n, SymWs w, SymRange g, double* __restrict
             ay += v.y;
         }
         // d = D of an even block count belongs to the lower block only
-        const int64_t dend = (even && g.d1 == D + 1 && (J - D + Mb) % Mb >= Mb / 2) ? D : g.d1;
+        const bool skipD = even && (J - D + Mb) % Mb >= Mb / 2;
         const double2* bp = reinterpret_cast<const double2*>(w.bpart) + s;
+        for (int k = 0; k < g.nch; ++k) {
+            const int64_t c = g.c0 + (int64_t)k * g.cs;
+            const int64_t d0 = 1 + c * per, d1e = 1 + (c + 1) * per < D + 1 ? 1 + (c + 1) * per : D + 1;
+            const int64_t d1 = (skipD && d1e == D + 1) ? D : d1e;
 #pragma unroll 8
-        for (int64_t d = g.d0; d < dend; ++d) {
-            const double2 v = __ldcs(bp + (size_t)(d - 1) * n);
-            bx += v.x;
-            by += v.y;
+            for (int64_t d = d0; d < d1; ++d) {
+                const double2 v = __ldcs(bp + (size_t)(d - 1) * n);
+                bx += v.x;
+                by += v.y;
+            }
         }
         part[2 * s] = ax - bx;
         part[2 * s + 1] = ay - by;
@@ -894,16 +898,14 @@ __global__ void k_sym_finish(int64_t n, SymWs w, const double* __restrict__ part
 #endif  // __CUDACC__
 
 BD_HD SymRange sym_range(int64_t n, int rank, int world) {
+    // chunks dealt round-robin: every rank gets near and far block distances
+    // alike (the per-pair image modes cluster at some distances), and the
+    // half-weight last distance (d = D for even Mb) lands on one rank only
     SymRange g;
-    const int64_t S = sym_chunks(n);
-    g.c0 = (int)((int64_t)rank * S / world);
-    g.c1 = (int)((int64_t)(rank + 1) * S / world);
-    const int64_t D = sym_D(n), per = sym_per(n), Mb = sym_blocks(n);
-    const int64_t a = 1 + (int64_t)g.c0 * per;  // chunk c starts at distance 1 + c per
-    const int64_t b = 1 + (int64_t)g.c1 * per;
-    g.d0 = a < D + 1 ? a : D + 1;
-    g.d1 = b < D + 1 ? b : D + 1;
-    if (g.c1 <= g.c0) g.d1 = g.d0;
+    const int64_t S = sym_chunks(n), Mb = sym_blocks(n);
+    g.c0 = rank;
+    g.cs = world;
+    g.nch = (sym_D(n) > 0 && rank < S) ? (int)((S - 1 - rank) / world + 1) : 0;  // no chunks without block pairs
     g.i0 = (int64_t)rank * Mb / world;
     g.i1 = (int64_t)(rank + 1) * Mb / world;
     return g;

@@ -684,10 +684,11 @@ int launch_sym_partial(const double* pos, const double* alpha, const double* mu,
     k_tie_scatter<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, w);
     k_tie_check<<<grid_for(n), 256, 0, st>>>(n, p.L, w);
     const SymRange g = sym_range(n, rank, world);
-    if (g.c1 > g.c0 || g.i1 > g.i0)
+    const int nch = g.nch;
+    if (nch > 0 || g.i1 > g.i0)
         timing_begin(st);
-        k_allpairs_sym<<<dim3((unsigned)sym_blocks(n), (unsigned)(1 + g.c1 - g.c0)), SY_CT, SY_SMEM, st>>>(
-            w, n, p.L, p.mi_lo, p.mi_hi, g.c0, g.i0, g.i1);
+        k_allpairs_sym<<<dim3((unsigned)sym_blocks(n), (unsigned)(1 + nch)), SY_CT, SY_SMEM, st>>>(
+            w, n, p.L, p.mi_lo, p.mi_hi, g.c0, g.cs, g.i0, g.i1);
         timing_end(st);
     k_sym_partial<<<grid_for(n), 256, 0, st>>>(n, w, g, part);
     return err_code(cudaGetLastError());
@@ -992,7 +993,8 @@ int bd_sym_shard(int64_t n, int rank, int world, int64_t* out) {
     if (n < 0 || world < 1 || rank < 0 || rank >= world || !out) return -(int)cudaErrorInvalidValue;
     const SymRange g = sym_range(n, rank, world);
     const int64_t D = sym_D(n);
-    const int64_t v[11] = {SY_BT, sym_blocks(n), D, sym_chunks(n), sym_per(n), g.c0, g.c1, g.d0, g.d1, g.i0, g.i1};
+    const int64_t v[11] = {SY_BT, sym_blocks(n), D, sym_chunks(n), sym_per(n), g.c0, g.cs, g.nch, 0,
+                           g.i0, g.i1};
     for (int k = 0; k < 11; ++k) out[k] = v[k];
     return 0;
 }

@@ -59,7 +59,7 @@ def sym_shard(n: int, rank: int, world: int) -> dict:
     needed): which unordered block pairs and diagonal blocks it evaluates."""
     out = (ctypes.c_int64 * 11)()
     check(lib().bd_sym_shard(int(n), int(rank), int(world), out), "bd_sym_shard")
-    keys = ("block", "blocks", "D", "chunks", "per", "c0", "c1", "d0", "d1", "i0", "i1")
+    keys = ("block", "blocks", "D", "chunks", "per", "c0", "cs", "nch", "reserved", "i0", "i1")
     return dict(zip(keys, (int(v) for v in out)))
 
 

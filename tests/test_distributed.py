@@ -98,10 +98,20 @@ def test_gloo_world2_sharded_forces_equal_full(n):
     assert res == {0: True, 1: True}
 
 
+def rank_distances(plan):
+    D, per = plan["D"], plan["per"]
+    out = []
+    for k in range(plan["nch"]):
+        c = plan["c0"] + k * plan["cs"]
+        out.extend(range(1 + c * per, min(1 + (c + 1) * per, D + 1)))
+    return out
+
+
 def sym_partial_np(pos, alpha, L, plan):
     """Numpy restatement of one rank's FAST-SYM partial P_r (slots = particle
     order): diagonal blocks [i0, i1) as directed pairs (receiver side only),
-    block pairs (I, I + d mod Mb) for d in [d0, d1) both sides (for even Mb,
+    block pairs (I, I + d mod Mb) for d in the rank's chunks (chunk c holds
+    d in [1 + c per, 1 + (c + 1) per), capped at D), both sides (for even Mb,
     d = D only for I < Mb / 2).  Exact reference min image (core.py:81-90)."""
     n = pos.shape[0]
     B, Mb, D = plan["block"], plan["blocks"], plan["D"]
@@ -125,7 +135,7 @@ def sym_partial_np(pos, alpha, L, plan):
         t[idx, idx] = 0.0
         P[s] += (alpha[s][None, :, None] * t).sum(1)
     even = Mb % 2 == 0
-    for d in range(plan["d0"], plan["d1"]):
+    for d in rank_distances(plan):
         for I in range(Mb):
             if even and d == D and I >= Mb // 2:
                 continue
@@ -179,10 +189,12 @@ def test_gloo_fast_sym_partials_allreduce_equal_full(n, world):
     for rank, rel, same, plan in res:
         assert rel <= 1e-12, (rank, rel, plan)
         assert same, rank
-    # the ranks' chunk and diagonal ranges tile [0, S) and [0, Mb)
+    # the ranks' distances and diagonal ranges tile [1, D] and [0, Mb)
     plans = [r[3] for r in sorted(res, key=lambda r: r[0])]  # by rank
-    assert plans[0]["c0"] == 0 and plans[-1]["c1"] == plans[0]["chunks"]
-    assert all(a["c1"] == b["c0"] and a["i1"] == b["i0"] for a, b in zip(plans, plans[1:]))
+    ds = sorted(d for p in plans for d in rank_distances(p))
+    assert ds == list(range(1, plans[0]["D"] + 1))
+    assert plans[0]["i0"] == 0 and plans[-1]["i1"] == plans[0]["blocks"]
+    assert all(a["i1"] == b["i0"] for a, b in zip(plans, plans[1:]))
 
 
 @pytest.mark.parametrize("n,world", [(131072, 8), (131072, 2), (1048576, 8), (262144, 4), (65536, 8)])
@@ -194,7 +206,7 @@ def test_sym_shard_balance(n, world):
     Mb, D = plans[0]["blocks"], plans[0]["D"]
     work = []
     for p in plans:
-        pairs = sum(Mb // 2 if (Mb % 2 == 0 and d == D) else Mb for d in range(p["d0"], p["d1"]))
+        pairs = sum(Mb // 2 if (Mb % 2 == 0 and d == D) else Mb for d in rank_distances(p))
         work.append(pairs + 0.5 * (p["i1"] - p["i0"]))
     total = sum(work)
     assert abs(total - (Mb * D - (Mb // 2 if Mb % 2 == 0 else 0) + 0.5 * Mb)) < 1e-9

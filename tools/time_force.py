@@ -80,15 +80,24 @@ if os.environ.get("SYM_SLICES"):
     eng = _Engine(sys_, None, bp, 0)
     part = torch.zeros((n, 2), dtype=torch.float64, device="cuda")
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    t1 = None
     for G in (1, 2, 4, 8):
-        worst = 0.0
+        times, ktimes = [], []
         for r in range(G):
             call = lambda: lib().bd_force_sym_partial(C.byref(eng.s), C.byref(bp), r, G, C.c_void_p(part.data_ptr()), st)
             call(); torch.cuda.synchronize()
+            lib().bd_timing_enable(3)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(3):
                 call()
             e1.record(); torch.cuda.synchronize()
-            worst = max(worst, e0.elapsed_time(e1) / 3)
-        print(f"G={G}: slowest rank's FAST-SYM partial {worst:.3f} ms")
+            kb = (C.c_float * 3)()
+            k = lib().bd_timing_read(kb, 3)
+            lib().bd_timing_enable(0)
+            times.append(e0.elapsed_time(e1) / 3)
+            ktimes.append(sum(kb[i] for i in range(k)) / max(k, 1))
+        t1 = t1 or times[0]
+        print(f"G={G}: per-rank FAST-SYM partial (setup + pair kernel + partial sums) max {max(times):.3f} "
+              f"min {min(times):.3f} ms; pair kernel alone max {max(ktimes):.3f} min {min(ktimes):.3f} ms; "
+              f"force-phase efficiency T1/(G max) = {t1 / (G * max(times)):.3f}", flush=True)
