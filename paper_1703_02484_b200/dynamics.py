@@ -346,15 +346,29 @@ class _SimulationBase:
     def _run_batch(self, steps: int) -> list:
         import torch
         self._bump_versions()  # host copies read before these steps go stale
-        stats = torch.zeros((steps, _abi.STATS_WORDS), dtype=torch.int64, device=self.sys.device)
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps + 1)]
+        # per-call buffers are kept (a step() per host round trip stays lean):
+        # the stats rows (every launch writes its row's status word first thing)
+        # and the timing events
+        cache = self.__dict__.setdefault("_batch_cache", {})
+        stats = cache.get(("stats", steps))
+        if stats is None:
+            stats = cache[("stats", steps)] = torch.zeros((steps, _abi.STATS_WORDS), dtype=torch.int64,
+                                                          device=self.sys.device)
+            cache[("host", steps)] = torch.empty((steps, _abi.STATS_WORDS), dtype=torch.int64).pin_memory()
+        host_t = cache[("host", steps)]
+        evs = cache.setdefault("events", [])
+        while len(evs) < 2 * steps + 2:
+            evs.append(torch.cuda.Event(enable_timing=True))
         evs[0].record()
         for j in range(steps):
             self._launch_force()
             evs[2 * j + 1].record()
             self._launch_driver(stats[j].data_ptr())
             evs[2 * j + 2].record()
-        host = stats.cpu().numpy()
+        host_t.copy_(stats, non_blocking=True)
+        evs[2 * steps + 1].record()
+        evs[2 * steps + 1].synchronize()
+        host = host_t.numpy()
         decoded = [_decode_stats(host[j]) for j in range(steps)]
         # the noise-call counter after the batch: from the last step's stats
         # when every step ran clean (no second device read), else from HBM
