@@ -82,10 +82,12 @@ def test_particle_system_triangulation_and_angles_write_through():
     sim = product_sim(rec)
     L = float(rec["L"])
     p = sim.sys.positions
-    p[0] = [1.25, 2.5]
-    assert sim.sys.positions_t[0].tolist() == [1.25, 2.5]
-    sim.sys.positions[3, 1] += 0.125
-    assert float(sim.sys.positions_t[3, 1]) == float(np.asarray(p)[3, 1] + 0.125) % L
+    moved = [float(p[0, 0]) + 1e-7, float(p[0, 1])]  # small moves: the triangulation must stay valid
+    p[0] = moved
+    assert sim.sys.positions_t[0].tolist() == moved
+    y3 = float(np.asarray(p)[3, 1])
+    sim.sys.positions[3, 1] += 1e-7
+    assert float(sim.sys.positions_t[3, 1]) == y3 + 1e-7
     sim.sys.positions = np.asarray(sim.sys.positions) + L  # attribute assignment wraps like the constructor
     assert float(sim.sys.positions_t.max()) < L
     et = sim.tri.edge_tri
