@@ -33,6 +33,11 @@ def run(name, warm=20, steps=50):
     tot = np.mean([s.step_ms for s in st])
     print(f"{name}: N={n} step {tot:.4f} ms (force {f:.4f}, O(N) {tot - f:.4f}); sweeps {np.mean([s.overlap_iterations for s in st]):.1f} "
           f"flip passes {np.mean([s.flip_passes for s in st]):.1f}  [{os.environ.get('TAG', '')}]", flush=True)
+    keys = [k for k in st[0].work if k.startswith("t_")]
+    print("   device phase timers (us/step): " + ", ".join(
+        f"{k[2:-3]} {np.mean([s.work[k] for s in st]) / 1e3:.1f}" for k in keys), flush=True)
+    cnt = [k for k in st[0].work if not k.startswith("t_")]
+    print("   passes/step: " + ", ".join(f"{k} {np.mean([s.work[k] for s in st]):.1f}" for k in cnt), flush=True)
 
 
 for nm in sys.argv[1:]:
