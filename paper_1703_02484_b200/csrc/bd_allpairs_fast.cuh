@@ -130,7 +130,19 @@ __global__ void k_sort_count(const double* __restrict__ pos, int64_t n, double L
 // segment of the cells and walks it in coalesced 32-cell chunks (8 loads in
 // flight); pass 1 sums the segments, one warp scans the 32 segment totals,
 // pass 2 writes the offsets (and zeroes the scatter cursors)
-__global__ void __launch_bounds__(1024) k_sort_scan(SortWs w, int64_t ncells) {
+__device__ void sort_scan_cta(SortWs w, int64_t ncells);
+
+__global__ void __launch_bounds__(1024) k_sort_scan(SortWs w, int64_t ncells) { sort_scan_cta(w, ncells); }
+
+// two independent scans in one launch: CTA 0 scans (w0, n0), CTA 1 (w1, n1)
+__global__ void __launch_bounds__(1024) k_sort_scan2(SortWs w0, int64_t n0, SortWs w1, int64_t n1) {
+    if (blockIdx.x == 0)
+        sort_scan_cta(w0, n0);
+    else
+        sort_scan_cta(w1, n1);
+}
+
+__device__ void sort_scan_cta(SortWs w, int64_t ncells) {
     __shared__ int64_t seg[32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t per = ((ncells + 31) / 32 + 31) & ~(int64_t)31;

@@ -282,6 +282,40 @@ BD_DEV bool tie_axis(const SymWs& w, int64_t n, double L, uint64_t T, int axis) 
     return false;
 }
 
+// the FAST-SYM setup's per-particle passes fused: the sort-cell count of
+// k_sort_count (alpha group, Morton cell) and the tie-bucket counts of
+// k_tie_count in one pass; the two scatters in another
+__global__ void k_sym_count(const double* __restrict__ pos, const double* __restrict__ alpha, int64_t n, double L,
+                            SortWs sw, SymWs w) {
+    const int G = 1 << sw.grid_log2;
+    const double inv = (double)G / L;
+    const double a_ref = alpha[0];
+    const int64_t B = sym_tie_buckets(n);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = pos[2 * i], y = pos[2 * i + 1];
+        int cx = (int)(x * inv), cy = (int)(y * inv);
+        cx = cx < 0 ? 0 : (cx >= G ? G - 1 : cx);
+        cy = cy < 0 ? 0 : (cy >= G ? G - 1 : cy);
+        const int c = (int)morton2((uint32_t)cx, (uint32_t)cy) + (!(alpha[i] == a_ref) ? G * G : 0);
+        sw.cell_of[i] = c;
+        atomicAdd(&sw.cell_off[c], 1);
+        atomicAdd(&w.tcnt[tie_bucket(x, L, B)], 1);
+        atomicAdd(&w.tcnt[B + tie_bucket(y, L, B)], 1);
+    }
+}
+
+__global__ void k_sym_scatter(const double* __restrict__ pos, int64_t n, double L, SortWs sw, SymWs w) {
+    const int64_t B = sym_tie_buckets(n);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = sw.cell_of[i];
+        sw.order[sw.cell_off[c] + atomicAdd(&sw.cell_cur[c], 1)] = (int32_t)i;
+        const double x = pos[2 * i], y = pos[2 * i + 1];
+        const int64_t bx = tie_bucket(x, L, B), by = B + tie_bucket(y, L, B);
+        w.tval[w.tcnt[bx] + atomicAdd(&w.tcur[bx], 1)] = x;
+        w.tval[w.tcnt[by] + atomicAdd(&w.tcur[by], 1)] = y;
+    }
+}
+
 __global__ void k_tie_check(int64_t n, double L, SymWs w) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         const SelS q = w.sel[s];

@@ -663,33 +663,32 @@ int launch_sym_partial(const double* pos, const double* alpha, const double* mu,
     SortWs sw = w.sort;
     sw.grid_log2 = sw.grid_log2 > 2 ? sw.grid_log2 - 1 : sw.grid_log2;
     const int64_t nc = 2 * ((int64_t)1 << (2 * sw.grid_log2));
+    // receivers that can meet an image tie (EDGE mode only for those): coordinate buckets
+    const int64_t nb = 2 * sym_tie_buckets(n);
     cudaError_t e = cudaMemsetAsync(sw.cell_off, 0, sizeof(int32_t) * (nc + 1), st);
     if (e != cudaSuccess) return err_code(e);
-    k_sort_count<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, sw, alpha);
-    k_sort_scan<<<1, 1024, 0, st>>>(sw, nc);
-    k_sort_scatter<<<grid_for(n), 256, 0, st>>>(n, sw);
-    k_sort_fix<<<grid_for(nc), 256, 0, st>>>(nc, sw);
-    k_sym_pack<<<(unsigned)sym_tiles(n), SY_TS, 0, st>>>(pos, alpha, mu, n, p.L, p.mi_lo, p.mi_hi, w);
-    // receivers that can meet an image tie (EDGE mode only for those)
-    const int64_t nb = 2 * sym_tie_buckets(n);
     e = cudaMemsetAsync(w.tcnt, 0, sizeof(int32_t) * (nb + 1), st);
     if (e != cudaSuccess) return err_code(e);
-    k_tie_count<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, w);
+    // sort + tie buckets: one counting pass, both scans in one launch, one scatter pass
+    k_sym_count<<<grid_for(n), 256, 0, st>>>(pos, alpha, n, p.L, sw, w);
     {
         SortWs tb = w.sort;
         tb.cell_off = w.tcnt;
         tb.cell_cur = w.tcur;
-        k_sort_scan<<<1, 1024, 0, st>>>(tb, nb);
+        k_sort_scan2<<<2, 1024, 0, st>>>(sw, nc, tb, nb);
     }
-    k_tie_scatter<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, w);
+    k_sym_scatter<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, sw, w);
+    k_sort_fix<<<grid_for(nc), 256, 0, st>>>(nc, sw);
+    k_sym_pack<<<(unsigned)sym_tiles(n), SY_TS, 0, st>>>(pos, alpha, mu, n, p.L, p.mi_lo, p.mi_hi, w);
     k_tie_check<<<grid_for(n), 256, 0, st>>>(n, p.L, w);
     const SymRange g = sym_range(n, rank, world);
     const int nch = g.nch;
-    if (nch > 0 || g.i1 > g.i0)
+    if (nch > 0 || g.i1 > g.i0) {
         timing_begin(st);
         k_allpairs_sym<<<dim3((unsigned)sym_blocks(n), (unsigned)(1 + nch)), SY_CT, SY_SMEM, st>>>(
             w, n, p.L, p.mi_lo, p.mi_hi, g.c0, g.cs, g.i0, g.i1);
         timing_end(st);
+    }
     k_sym_partial<<<grid_for(n), 256, 0, st>>>(n, w, g, part);
     return err_code(cudaGetLastError());
 }
