@@ -85,6 +85,7 @@ def _protos():
         "bd_verlet_build": ([c_vp, c_i64, c_d, c_d, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp], c_int),
         "bd_probe_fp64": ([c_i64, c_vp, c_vp, P(c_d)], c_int),
         "bd_probe_barrier": ([c_i64, c_int, c_int, c_int, c_vp, c_vp, P(c_d)], c_int),
+        "bd_probe_exact_arith": ([c_u64, c_i64, c_vp, c_vp], c_int),
         "bd_brute_overlaps": ([c_vp, c_i64, c_d, c_d, c_vp, c_vp], c_int),
         "bd_normals": ([c_u64, c_u64, c_u64, c_u64, c_i64, c_vp, c_vp], c_int),
         "bd_force": ([P(BdState), P(BdParams), c_vp], c_int),

@@ -1194,6 +1194,74 @@ int bd_probe_fp64(int64_t iters, double* out, void* stream, double* flops_out) {
     return err_code(cudaGetLastError());
 }
 
+// ---- check of the branch-free IEEE sqrt / division of the EXACT kernel
+// (bd_allpairs.cuh: sqrt_rn_inrange, div_rn_inrange) against sqrt() and '/'
+// on n generated operand sets (tests/test_exact_fastpath_gpu.py).  Operands:
+// random mantissas with exponents over the whole guarded range, perfect
+// squares and products of short mantissas (exact roots and quotients) and
+// one ulp either side of them, and the kernel's own shape num / (r2 sqrt(r2)).
+// bad[0] = mismatches, bad[1..2] = the bits of the first offending operands,
+// bad[3..6] = mismatches of sqrt, a / b, r2 sqrt(r2), num / den.
+BD_DEV uint64_t probe_mix(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+BD_DEV double probe_make(uint64_t mant, int ex) {  // 1.mant * 2^ex
+    return __longlong_as_double((long long)(((uint64_t)(ex + 1023) << 52) | (mant & 0xfffffffffffffull)));
+}
+
+BD_DEV void probe_cmp(double got, double want, double a, double b, unsigned long long* bad, int which) {
+    if (dbits(got) != dbits(want)) {
+        atomicAdd(&bad[3 + which], 1ull);
+        if (atomicAdd(&bad[0], 1ull) == 0) {
+            bad[1] = dbits(a);
+            bad[2] = dbits(b);
+        }
+    }
+}
+
+__global__ void k_probe_exact_arith(uint64_t seed, int64_t n, unsigned long long* bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t h1 = probe_mix(seed ^ (uint64_t)(3 * i)), h2 = probe_mix(seed ^ (uint64_t)(3 * i + 1));
+        const uint64_t h3 = probe_mix(seed ^ (uint64_t)(3 * i + 2));
+        const int ea = (int)(h3 % 401) - 200, eb = (int)((h3 >> 20) % 401) - 200;
+        const int kind = (int)(h3 >> 40) & 7;
+        const int ulps = (int)((h3 >> 44) & 3) - 1;  // -1, 0, +1, +2
+        double a = probe_make(h1, ea), b = probe_make(h2, eb);
+        if (kind == 1 || kind == 2) {  // short mantissas: exact squares / exact quotients (+- ulps)
+            const double ra = probe_make(h1 & ~((1ull << 26) - 1), ea / 2);
+            const double rb = probe_make(h2 & ~((1ull << 26) - 1), eb / 2);
+            a = __longlong_as_double((long long)(dbits(ra * ra) + (int64_t)ulps));
+            if (kind == 2) {
+                b = rb;
+                a = __longlong_as_double((long long)(dbits(ra * rb) + (int64_t)ulps));
+            }
+        } else if (kind == 3) {  // powers of two and all-ones mantissas
+            a = probe_make((h1 & 1) ? 0ull : ~0ull, ea);
+            b = probe_make((h2 & 1) ? 0ull : ~0ull, eb);
+        }
+        probe_cmp(sqrt_rn_inrange(a), sqrt(a), a, a, bad, 0);
+        probe_cmp(div_rn_inrange(a, b), a / b, a, b, bad, 1);
+        // the EXACT kernel's operands: num / (r2 sqrt(r2)), r2 from a square sum
+        const double r2 = fabs(a) * 1e-100 < 1.0 ? fabs(a) : 1.0 / fabs(a);
+        if (in_range(r2)) {
+            const double den = r2 * sqrt_rn_inrange(r2);
+            probe_cmp(den, r2 * sqrt(r2), r2, r2, bad, 2);
+            probe_cmp(div_rn_inrange(b, den), b / den, b, den, bad, 3);
+        }
+    }
+}
+
+int bd_probe_exact_arith(uint64_t seed, int64_t n, void* bad, void* stream) {
+    init_device_info();
+    cudaMemsetAsync(bad, 0, 7 * sizeof(unsigned long long), (cudaStream_t)stream);
+    k_probe_exact_arith<<<g_num_sms * 8, 256, 0, (cudaStream_t)stream>>>(seed, n, (unsigned long long*)bad);
+    return err_code(cudaGetLastError());
+}
+
 // ---- grid-barrier probe (measurement only): latency of the cooperative
 // grid.sync the step drivers end every phase with (tools/probe_barrier.py)
 __global__ void k_probe_gridsync(int64_t iters, int mode, unsigned* bar) {
