@@ -21,8 +21,9 @@ Extra keyword arguments of LongRangeSimulation (not in the reference):
   precision    "exact" (bit-identical to the reference), "fast-sym" (FAST
                arithmetic, each unordered pair's r^-3 evaluated once for both
                directions; sharded by block pairs + all-reduce; workspace
-               ~ n^2/64 bytes: 18 GB at 1M particles), "auto" (fast-sym
-               while that fits half the free HBM, else fast) or "fast" (sorted,
+               ~ n^2/64 bytes: 18 GB at 1M particles), "auto" (exact up to
+               4,096 particles, then fast-sym while that fits half the free
+               HBM, else fast) or "fast" (sorted,
                FMA + rsqrt all-pairs; |dF|/|F| ~1e-13);
   skin         Verlet skin for the short-range force (default sigma / 2).
 """
@@ -47,6 +48,7 @@ RESOLVE_FRAC = 1.0 - 1e-9  # dynamics.py:39
 FORCE_MODES = {"long-range": _abi.BD_FORCE_LR, "short-range": _abi.BD_FORCE_SR, "long+short": _abi.BD_FORCE_LRSR}
 PRECISIONS = {"exact": _abi.BD_LR_EXACT, "fast": _abi.BD_LR_FAST, "fast-sym": _abi.BD_LR_FAST_SYM}
 AUTO_SYM_FREE_FRACTION = 0.5  # precision="auto": FAST-SYM while its workspace (~n^2/64 B) fits half the free HBM
+AUTO_EXACT_MAX_N = 4096  # precision="auto": EXACT up to here (B200: 0.033 ms at 1,024 vs 0.17 for FAST-SYM's launch chain)
 
 
 @dataclass
@@ -444,11 +446,14 @@ class LongRangeSimulation(_SimulationBase):
             raise BrownsimError(f"unknown force model {force!r}; have {sorted(FORCE_MODES)}")
         if force != "long-range" and params.r_cutoff is None:
             raise BrownsimError("short-range force requires params.r_cutoff")
-        if precision == "auto":  # FAST-SYM while its partial buffer stays modest, else FAST
+        if precision == "auto":  # EXACT for small systems; FAST-SYM while its partial buffer stays modest, else FAST
             import torch
             free, _ = torch.cuda.mem_get_info(sys.device)
-            precision = "fast-sym" if lib().bd_long_range_workspace_bytes_for(sys.n, _abi.BD_LR_FAST_SYM) \
-                <= AUTO_SYM_FREE_FRACTION * free else "fast"
+            if sys.n <= AUTO_EXACT_MAX_N:
+                precision = "exact"
+            else:
+                precision = "fast-sym" if lib().bd_long_range_workspace_bytes_for(sys.n, _abi.BD_LR_FAST_SYM) \
+                    <= AUTO_SYM_FREE_FRACTION * free else "fast"
         if precision not in PRECISIONS:
             raise BrownsimError(f"unknown precision {precision!r}; have {sorted(PRECISIONS) + ['auto']}")
         self.force_model = force
