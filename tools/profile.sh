@@ -17,7 +17,8 @@ for what in $P; do
         --metrics sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum \
         -o gpurun_out/prof_allpairs_sym python tools/prof_force.py 131072 fast-sym 2 > gpurun_out/ncu_aps.log 2>&1 ;;
     exact)     # EXACT all-pairs kernel (N = 131,072)
-      timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k k_allpairs -c 1 \
+      timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k k_allpairs -c 1 \
+        --metrics sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum \
         -o gpurun_out/prof_allpairs_exact python tools/prof_force.py 131072 exact 1 > gpurun_out/ncu_apx.log 2>&1 ;;
     step)      # persistent step kernel (cfg3 state after warm-up)
       timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_step_tri_grid -s 2 -c 1 \
