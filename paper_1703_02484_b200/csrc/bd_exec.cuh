@@ -127,7 +127,23 @@ struct ExecGrid {
     BD_DEV u64 fetch_add64(u64* p, u64 v) { return atomicAdd(p, v); }
     BD_DEV u64 append(u64* p) { return warp_append(p); }  // list slot, one atomic per warp
     BD_DEV uint32_t exch32(uint32_t* p, uint32_t v) { return atomicExch(p, v); }
-    BD_DEV u64 ld(const u64* p) const { return ld_volatile(p); }
+#ifndef BD_GRID_LD_BCAST
+#define BD_GRID_LD_BCAST 1
+#endif
+    // a control word read after a barrier (uniform: every thread calls it):
+    // one load per CTA, broadcast through shared memory, instead of every
+    // warp of the grid loading the same L2 line right after the barrier
+    BD_DEV u64 ld(const u64* p) const {
+#if BD_GRID_LD_BCAST
+        __shared__ u64 bc;
+        __syncthreads();  // earlier readers of bc are done
+        if (threadIdx.x == 0) bc = ld_volatile(p);
+        __syncthreads();
+        return bc;
+#else
+        return ld_volatile(p);
+#endif
+    }
 
     // in-place exclusive scan of a[0..n) (int32), a[n] = total; ends with a barrier
     BD_DEV void exclusive_scan(int32_t* a, int64_t n) {
