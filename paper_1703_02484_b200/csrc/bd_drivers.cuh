@@ -55,6 +55,52 @@ BD_HD bool check_finite(X& x, Red<X>& R, Ctx& c, bd_stats_t* out) {
     return true;
 }
 
+// check_singular (when err is given) + check_finite + save_state
+// (triangulation.py:158-160, with the image counters; `backup`) as ONE phase: the
+// checks only read, the backup only writes the backup arrays, so a single
+// barrier serves all three (the singular check keeps precedence)
+template <class X>
+BD_HD bool check_and_backup(X& x, Red<X>& R, Ctx& c, const int64_t* err, bd_stats_t* out, bool backup = true) {
+    u64* r = R.open();  // scratch[0] / scratch[1] = ~0 since driver_enter
+    for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
+        const bool bs = err && err[i] != 0;
+        const bool bf = !(isfinite(c.s.force[2 * i]) && isfinite(c.s.force[2 * i + 1]));
+        if (bs) x.umin(&c.w.ctl->scratch[1], (u64)i);
+        if (bf) x.umin(&c.w.ctl->scratch[0], (u64)i);
+        R.add((u64)bs | ((u64)bf << 32));
+    }
+    if (backup) {
+        ph_tri_copy(x, c.s.tri, c.s.tri_backup);
+        if (c.s.image)
+            for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.w.image_bk[i] = c.s.image[i];
+    }
+    const u64 v = R.close(r);
+    if (v & 0xffffffffull) {
+        if (x.leader()) {
+            const int64_t i = (int64_t)c.w.ctl->scratch[1];
+            c.w.ctl->status = BD_ERR_SINGULAR;
+            c.w.ctl->err_i = (u64)i;
+            c.w.ctl->err_k = (u64)(err[i] - 1);
+            out->status = BD_ERR_SINGULAR;
+            out->err_i = i;
+            out->err_k = err[i] - 1;
+        }
+        x.sync();
+        return true;
+    }
+    if (v >> 32) {
+        if (x.leader()) {
+            c.w.ctl->status = BD_ERR_STEPFAIL;
+            c.w.ctl->err_i = c.w.ctl->scratch[0];
+            out->status = BD_ERR_STEPFAIL;
+            out->err_i = (int64_t)c.w.ctl->scratch[0];
+        }
+        x.sync();
+        return true;
+    }
+    return false;
+}
+
 template <class X>
 BD_HD bool driver_enter(X& x, Red<X>& R, Ctx& c, bd_stats_t* out) {
     if (x.leader()) {
@@ -106,7 +152,7 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
     const int64_t t_enter = now_ns();
     if (!driver_enter(x, R, c, out)) return;
     const int64_t rebuilds0 = c.s.vl_meta ? c.s.vl_meta[2] : 0;
-    if (c.p.force_mode != BD_FORCE_SR && check_singular(x, R, c, c.s.force_err, out)) return;
+    if (c.p.force_mode == BD_FORCE_LRSR && check_singular(x, R, c, c.s.force_err, out)) return;
     if (c.p.force_mode != BD_FORCE_LR) {
         // short-range force over a Verlet list kept fresh by the rebuild rule
         const bool stale = vl_stale(x, R, c);
@@ -121,12 +167,8 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
             c.s.force[i] = add ? c.s.force[i] + c.w.sr_force[i] : c.w.sr_force[i];
         x.sync();
     }
-    if (check_finite(x, R, c, out)) return;
-    // save_state (triangulation.py:158-160) + image counters
-    ph_tri_copy(x, c.s.tri, c.s.tri_backup);
-    if (c.s.image)
-        for (int64_t i = x.tid(); i < 2 * c.p.n; i += x.nth()) c.w.image_bk[i] = c.s.image[i];
-    x.sync();
+    // LR: the long-range singularity check here; + check_finite + save_state
+    if (check_and_backup(x, R, c, c.p.force_mode == BD_FORCE_LR ? c.s.force_err : nullptr, out)) return;
 
     double dt_try = c.p.dt;
     int64_t rollbacks = 0, iters = 0, repairs = 0, flip_passes = 0;
@@ -267,8 +309,7 @@ BD_HD void step_verlet(X& x, Ctx& c, bd_stats_t* out) {
         return;
     }
     sr_forces(x, c, c.s.force, c.s.force_err);
-    if (check_singular(x, R, c, c.s.force_err, out)) return;
-    if (check_finite(x, R, c, out)) return;
+    if (check_and_backup(x, R, c, c.s.force_err, out, false)) return;  // check_singular + check_finite
     ph_integrate(x, R, c, c.p.dt);
     c.call++;
     for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) c.s.overlap_flags[i] = 0;
