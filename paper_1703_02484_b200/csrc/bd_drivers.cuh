@@ -128,22 +128,11 @@ BD_HD int maintain_t(X& x, Red<X>& R, Ctx& c, int64_t* repairs, int64_t* flip_pa
 }
 
 template <class X, class PS>
-BD_HD int64_t correct_overlaps_t(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri) {
-    const int64_t t0 = now_ns();
-    const int64_t r = correct_overlaps(x, R, c, ps, tri);
-    c.work[WK_T_OVERLAP] += now_ns() - t0;
+BD_HD int64_t correct_overlaps_t(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri, bool edge_inc = false) {
+    const int64_t t0 = now_ns(), ti0 = c.work[WK_T_INCIDENCE];
+    const int64_t r = correct_overlaps(x, R, c, ps, tri, edge_inc);
+    c.work[WK_T_OVERLAP] += now_ns() - t0 - (c.work[WK_T_INCIDENCE] - ti0);  // lazy incidence builds: their own timer
     return r;
-}
-
-template <class X>
-BD_HD void build_edge_incidence_t(X& x, Ctx& c) {
-    // the lists depend on edge_v only, which only flips (and a rollback)
-    // change: an outer round whose maintenance flipped nothing reuses them
-    if (c.inc_flips == c.work[WK_FLIPS]) return;
-    const int64_t t0 = now_ns();
-    build_edge_incidence(x, c);
-    c.inc_flips = c.work[WK_FLIPS];
-    c.work[WK_T_INCIDENCE] += now_ns() - t0;
 }
 
 template <class X>
@@ -190,8 +179,7 @@ BD_HD void step_tri_after_force(X& x, Ctx& c, bd_stats_t* out) {
             for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) c.s.overlap_flags[i] = 0;
             int64_t outer;
             for (outer = 0; outer < c.p.max_overlap_iters; ++outer) {
-                build_edge_incidence_t(x, c);
-                const int64_t ri = correct_overlaps_t(x, R, c, EdgePairs{c.s.tri.edge_v, c.s.tri.ne}, true);
+                const int64_t ri = correct_overlaps_t(x, R, c, EdgePairs{c.s.tri.edge_v, c.s.tri.ne}, true, true);
                 if (ri < 0) break;
                 iters += ri;
                 if (ri == 0) break;

@@ -803,11 +803,25 @@ BD_HD void build_edge_incidence(X& x, Ctx& c) {
     build_incidence(x, c.p.n, ps, c.w.inc_off, c.w.inc_cur, c.w.inc, c.work);
 }
 
+// the edge incidence lists when stale: they depend on edge_v only, which
+// only flips (and a rollback) change
+template <class X>
+BD_HD void build_edge_incidence_t(X& x, Ctx& c) {
+    if (c.inc_flips == c.work[WK_FLIPS]) return;
+    const int64_t t0 = now_ns();
+    build_edge_incidence(x, c);
+    c.inc_flips = c.work[WK_FLIPS];
+    c.work[WK_T_INCIDENCE] += now_ns() - t0;
+}
+
 // correct_overlaps (dynamics.py:97-133) over a fixed pair set with its
 // incidence lists in w.inc_off / w.inc; `tri` -> crossings feed
 // apply_crossings (dynamics.py:127-129).  Returns sweeps, -1 on non-convergence.
+// edge_inc: ps are the triangulation edges and their incidence lists are
+// built here, only once a pass finds an overlap (most calls after a
+// maintenance round find none and never need them)
 template <class X, class PS>
-BD_HD int64_t correct_overlaps(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri) {
+BD_HD int64_t correct_overlaps(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri, bool edge_inc = false) {
     const double L = c.p.L, sigma = c.p.sigma, thresh = sigma * (1.0 - 1e-9), cap = c.p.cap;
     double* pos = c.s.pos;
     const int64_t m = ps.count();
@@ -840,6 +854,7 @@ BD_HD int64_t correct_overlaps(X& x, Red<X>& R, Ctx& c, const PS& ps, bool tri) 
             return iterations;
         }
         iterations++;
+        if (edge_inc) build_edge_incidence_t(x, c);
         c.work[WK_OVL_APPLY]++;
         u64* rc = R.open();
         for (int64_t i = x.tid(); i < c.p.n; i += x.nth()) {
