@@ -406,11 +406,9 @@ BD_HD bool ph_edge_inversion(X& x, Red<X>& R, Ctx& c) {
     return R.close(r) != 0;
 }
 
-// signed_area2 <= 0 per triangle; returns #inverted
+// signed_area2 <= 0 per triangle (into w.tinv), added to the open reduction
 template <class X>
-BD_HD u64 ph_inverted_tris(X& x, Red<X>& R, Ctx& c) {
-    c.work[WK_AREA_PASS]++;
-    u64* r = R.open();
+BD_HD void inverted_tris_body(X& x, Red<X>& R, Ctx& c, int shift) {
     const bd_tri_t& T = c.s.tri;
     for (int64_t t = x.tid(); t < T.nt; t += x.nth()) {
         V2 xy[3];
@@ -419,8 +417,37 @@ BD_HD u64 ph_inverted_tris(X& x, Red<X>& R, Ctx& c) {
         const double e2x = xy[2].x - xy[0].x, e2y = xy[2].y - xy[0].y;
         const bool inv = e1x * e2y - e1y * e2x <= 0.0;
         c.w.tinv[t] = (uint8_t)inv;
-        R.add((u64)inv);
+        R.add((u64)inv << shift);
     }
+}
+
+// signed_area2 <= 0 per triangle; returns #inverted
+template <class X>
+BD_HD u64 ph_inverted_tris(X& x, Red<X>& R, Ctx& c) {
+    c.work[WK_AREA_PASS]++;
+    u64* r = R.open();
+    inverted_tris_body(x, R, c, 0);
+    return R.close(r);
+}
+
+// edge_inversion_present and the first inverted-triangle pass of
+// repair_inversions in one phase (both only read positions and topology):
+// low word = inverted edges, high word = inverted triangles
+template <class X>
+BD_HD u64 ph_edge_inversion_and_area(X& x, Red<X>& R, Ctx& c) {
+    c.work[WK_EDGE_INV]++;
+    c.work[WK_AREA_PASS]++;
+    u64* r = R.open();
+    const bd_tri_t& T = c.s.tri;
+    const double* prev = c.s.prev;
+    const double* cur = c.s.pos;
+    for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
+        const int64_t a = T.edge_v[2 * e], b = T.edge_v[2 * e + 1];
+        const double d0x = mi_exact(prev[2 * b] - prev[2 * a], c.p), d0y = mi_exact(prev[2 * b + 1] - prev[2 * a + 1], c.p);
+        const double d1x = mi_exact(cur[2 * b] - cur[2 * a], c.p), d1y = mi_exact(cur[2 * b + 1] - cur[2 * a + 1], c.p);
+        R.add((u64)(d0x * d1x + d0y * d1y < 0.0));
+    }
+    inverted_tris_body(x, R, c, 32);
     return R.close(r);
 }
 
@@ -673,11 +700,13 @@ BD_HD int64_t restore_delaunay(X& x, Red<X>& R, Ctx& c, int64_t max_passes) {
 // given, the reference's RepairResult.passes to *passes
 template <class X>
 BD_HD int repair_inversions(X& x, Red<X>& R, Ctx& c, int64_t max_passes, int64_t* flips, bool use_prev = true,
-                            int64_t* passes = nullptr) {
+                            int64_t* passes = nullptr, int64_t inverted0 = -1) {
     bd_tri_t& T = c.s.tri;
     for (int64_t pass = 0; pass < max_passes; ++pass) {
         if (passes) *passes = pass;
-        if (ph_inverted_tris(x, R, c) == 0) return 0;
+        // inverted0: the first pass's count (and w.tinv) already computed by the caller
+        const u64 ninv = pass == 0 && inverted0 >= 0 ? (u64)inverted0 : ph_inverted_tris(x, R, c);
+        if (ninv == 0) return 0;
         c.work[WK_FLAG_PASS]++;
         for (int64_t e = x.tid(); e < T.ne; e += x.nth()) {
             V2 q[4];
@@ -703,8 +732,9 @@ BD_HD int repair_inversions(X& x, Red<X>& R, Ctx& c, int64_t max_passes, int64_t
 // (dynamics.py:206-214 and :236-242): 0 ok, 1 rollback, -1 error
 template <class X>
 BD_HD int maintain(X& x, Red<X>& R, Ctx& c, int64_t* repairs, int64_t* flip_passes) {
-    if (ph_edge_inversion(x, R, c)) return 1;
-    const int rr = repair_inversions(x, R, c, 10, repairs);
+    const u64 v = ph_edge_inversion_and_area(x, R, c);
+    if (v & 0xffffffffull) return 1;
+    const int rr = repair_inversions(x, R, c, 10, repairs, true, nullptr, (int64_t)(v >> 32));
     if (rr) return rr;
     const int64_t p = restore_delaunay(x, R, c, 1000);
     if (p < 0) return -1;
