@@ -327,7 +327,10 @@ def run_ours(args):
     achieved = FLOPS_PER_PAIR * pairs / (f_ms * 1e-3) / 1e12
     peak = fp64 if fp64 else 37.2
     cpu = None
-    if not args.no_cpu_baseline:
+    if world > 1:  # the CPU baseline is taken on rank 0 of the N = 1 run only
+        cpu = {"value": None, "unit": "particle-steps/s", "cores": None, "kind": "port",
+               "sample": "not measured at N > 1 (see the N = 1 line)"}
+    elif not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
             t_force, t_maint, ns = cpu_step_sample(box, pos, alpha, mu, tri0, sys_first_forces(n, pos, alpha, mu,
