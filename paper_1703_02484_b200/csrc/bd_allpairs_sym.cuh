@@ -888,6 +888,7 @@ __global__ void k_sym_partial(int64_t n, SymWs w, SymRange g, double* __restrict
         // diagonal block, then the source-side distances of those chunks ascending
         double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
         const double2* ap = reinterpret_cast<const double2*>(w.apart) + s;
+#pragma unroll 8
         for (int k = 0; k < g.nch; ++k) {
             const double2 v = __ldcs(ap + (size_t)(g.c0 + k * g.cs) * n);
             ax += v.x;
@@ -902,12 +903,16 @@ __global__ void k_sym_partial(int64_t n, SymWs w, SymRange g, double* __restrict
         // d = D of an even block count belongs to the lower block only
         const bool skipD = even && (J - D + Mb) % Mb >= Mb / 2;
         const double2* bp = reinterpret_cast<const double2*>(w.bpart) + s;
-        for (int k = 0; k < g.nch; ++k) {
-            const int64_t c = g.c0 + (int64_t)k * g.cs;
-            const int64_t d0 = 1 + c * per, d1e = 1 + (c + 1) * per < D + 1 ? 1 + (c + 1) * per : D + 1;
-            const int64_t d1 = (skipD && d1e == D + 1) ? D : d1e;
+        // the distances of this rank's chunks in ascending order as one flat
+        // loop (independent loads in flight; the same addition order)
+        const int64_t dmax = skipD ? D - 1 : D;
+        const int per32 = (int)per, nf = g.nch * per32;
 #pragma unroll 8
-            for (int64_t d = d0; d < d1; ++d) {
+        for (int f = 0; f < nf; ++f) {
+            const int q = f / per32;
+            const int64_t c = g.c0 + (int64_t)q * g.cs;
+            const int64_t d = 1 + c * per + (f - q * per32);
+            if (d <= dmax) {
                 const double2 v = __ldcs(bp + (size_t)(d - 1) * n);
                 bx += v.x;
                 by += v.y;
