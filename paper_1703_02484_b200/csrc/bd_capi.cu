@@ -57,7 +57,7 @@ int64_t block_max_n() {
     static int64_t v = -1;
     if (v < 0) {
         const char* e = getenv("BD_BLOCK_MAX_N");
-        v = e ? atoll(e) : 1536;
+        v = e ? atoll(e) : 768;  // one-CTA drivers up to here (B200: 0.129 vs 0.153 ms per O(N) step at 512, 0.192 vs 0.184 at 1,024)
     }
     return v;
 }
