@@ -735,12 +735,14 @@ int launch_force(const bd_state_t* s, const bd_params_t* p, cudaStream_t st) {
 // From this many particles the triangulation step runs as one 1024-thread CTA
 // per SM (k_step_tri_grid_big) instead of 4 x 256: the same threads, a
 // quarter of the barrier arrivals (grid.sync 1.27 vs 1.63 us): cfg3 O(N)
-// step 0.69 -> 0.63 ms.  BD_BIG_MIN_N overrides (0: off).
+// step 0.69 -> 0.63 ms; from 32k since the per-CTA control-word reads
+// (O(N) step at 16k / 32k / 48k / 64k: 0.277 vs 0.248, 0.351 vs 0.357,
+// 0.378 vs 0.476, 0.577 vs 0.616 ms).  BD_BIG_MIN_N overrides (0: off).
 int64_t big_min_n() {
     static int64_t v = -1;
     if (v < 0) {
         const char* e = getenv("BD_BIG_MIN_N");
-        v = e ? atoll(e) : 100000;
+        v = e ? atoll(e) : 32768;
     }
     return v;
 }

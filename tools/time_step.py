@@ -11,7 +11,8 @@ import torch  # noqa: E402
 
 C0 = [(0.5, 3.0, 3.0), (0.5, -3.0, -1.5)]
 CFG = {"n256": (256, 0.3, "long-range", "exact", 0), "n512": (512, 0.3, "long-range", "exact", 0),
-       "n1536": (1536, 0.3, "long-range", "exact", 0),
+       "n1536": (1536, 0.3, "long-range", "exact", 0), "n32768": (32768, 0.3, "long-range", "fast-sym", 0),
+       "n49152": (49152, 0.3, "long-range", "fast-sym", 0),
        "cfg1": (1024, 0.3, "long-range", "exact", 0), "cfg2": (16384, 0.3, "short-range", "exact", 0),
        "n4096": (4096, 0.3, "long-range", "exact", 0), "n8192": (8192, 0.3, "long-range", "fast-sym", 0),
        "cfg5": (65536, 0.3, "long+short", "fast-sym", 0), "cfg3": (131072, 0.3, "long-range", "fast-sym", 0)}
