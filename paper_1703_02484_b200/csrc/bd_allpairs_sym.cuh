@@ -655,10 +655,10 @@ BD_DEV void sym_issue(const SymWs& w, int64_t n, int64_t t, unsigned char* smem,
 }
 
 // grid (Mb, 1 + chunks), SY_CT threads.  CTA (x, y): receiver block I = x;
-// y = 0: the diagonal block J = I (directed, receiver side only) when
-// I is in [i0, i1), else nothing; y >= 1: distance chunk c = chunk0 + (y - 1) cstep.
-// The diagonal row comes first so its short CTAs interleave with the rest
-// instead of forming a tail.  Warp v of block I owns slots
+// y = chunks (the last row): the diagonal block J = I (directed, receiver
+// side only) when I is in [i0, i1), else nothing; y < chunks: distance
+// chunk c = chunk0 + y cstep.  The diagonal row's short CTAs come last and
+// fill the final wave.  Warp v of block I owns slots
 // I*SY_BT + 32 SY_R v + lane + 32 m, m < SY_R.  Its receiver sums over the
 // chunk go to apart[c]; the CTA's source-side sums of each tile of block
 // J = I + d go to bpart[d - 1].  A CTA barrier ends every tile; the stage
@@ -676,9 +676,14 @@ __global__ void __launch_bounds__(SY_CT, BD_SY_MINB) k_allpairs_sym(SymWs w, int
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t Mb = sym_blocks(n), D = sym_D(n);
     const int64_t I = blockIdx.x;
-    const bool diag = blockIdx.y == 0;
+#ifndef BD_SY_DIAG_LAST
+#define BD_SY_DIAG_LAST 1
+#endif
+    // the diagonal row: last (its short CTAs fill the final wave: 9.13 ->
+    // 9.11 ms at cfg3) or first (BD_SY_DIAG_LAST=0)
+    const bool diag = BD_SY_DIAG_LAST ? blockIdx.y == gridDim.y - 1 : blockIdx.y == 0;
     if (diag && (I < i0 || I >= i1)) return;
-    const int chunk = diag ? SY_S : chunk0 + ((int)blockIdx.y - 1) * cstep;
+    const int chunk = diag ? SY_S : chunk0 + ((int)blockIdx.y - (BD_SY_DIAG_LAST ? 0 : 1)) * cstep;
     const LaneAcc acc{accs + threadIdx.x};
 
     int64_t slot[SY_R];
