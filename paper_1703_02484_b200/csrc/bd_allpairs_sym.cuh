@@ -58,7 +58,7 @@ struct SrcS {  // one source as the pair loop sees it (shared-memory stage: xy a
 struct alignas(16) SelS {  // receiver image selector (axis_select of both axes)
     double cx_le, cx_gt, cy_le, cy_gt;
     uint64_t Tx, Ty, amb;
-    uint64_t tie;  // bit 0 / 1: some source lies within eps of the x / y breakpoint (k_tie_check)
+    uint64_t tie;  // bit 0 / 1: some source lies within eps of the x / y breakpoint (k_sym_pack)
 };
 
 // 4 receivers per lane in CTAs of 4 warps (each source read from shared
@@ -158,7 +158,10 @@ BD_HD SymWs sym_ws_carve(void* base, int64_t n) {
 
 #if defined(__CUDACC__)
 
-// one CTA per SY_TS tile of slots: sources, receiver selectors, tile box
+BD_DEV bool tie_axis(const SymWs& w, int64_t n, double L, uint64_t T, int axis);
+
+// one CTA per SY_TS tile of slots: sources, receiver selectors (with their
+// tie bits: the coordinate buckets are filled by k_sym_scatter), tile box
 __global__ void __launch_bounds__(SY_TS) k_sym_pack(const double* __restrict__ pos, const double* __restrict__ alpha,
                                                     const double* __restrict__ mu, int64_t n, double L, double lo,
                                                     double hi, SymWs w) {
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(SY_TS) k_sym_pack(const double* __restrict__ p
         q.Tx = sx.T;
         q.Ty = sy.T;
         q.amb = (uint64_t)(sx.amb || sy.amb);
-        q.tie = 0;
+        q.tie = (uint64_t)tie_axis(w, n, L, q.Tx, 0) | ((uint64_t)tie_axis(w, n, L, q.Ty, 1) << 1);
         w.sel[s] = q;
         xmin = xmax = dbits(x);
         ymin = ymax = dbits(y);
@@ -316,12 +319,6 @@ __global__ void k_sym_scatter(const double* __restrict__ pos, int64_t n, double 
     }
 }
 
-__global__ void k_tie_check(int64_t n, double L, SymWs w) {
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
-        const SelS q = w.sel[s];
-        w.sel[s].tie = (uint64_t)tie_axis(w, n, L, q.Tx, 0) | ((uint64_t)tie_axis(w, n, L, q.Ty, 1) << 1);
-    }
-}
 
 // r^-3 from r^2: y0 = MUFU.RSQ64H (~2^-22), e = 1 - r2 y0^2,
 // r^-3 = y0^3 (1 + 1.5 e + 1.875 e^2) (+ O(e^3) ~ 1e-19)

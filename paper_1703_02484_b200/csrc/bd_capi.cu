@@ -680,7 +680,6 @@ int launch_sym_partial(const double* pos, const double* alpha, const double* mu,
     k_sym_scatter<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, sw, w);
     k_sort_fix<<<grid_for(nc), 256, 0, st>>>(nc, sw);
     k_sym_pack<<<(unsigned)sym_tiles(n), SY_TS, 0, st>>>(pos, alpha, mu, n, p.L, p.mi_lo, p.mi_hi, w);
-    k_tie_check<<<grid_for(n), 256, 0, st>>>(n, p.L, w);
     const SymRange g = sym_range(n, rank, world);
     const int nch = g.nch;
     if (nch > 0 || g.i1 > g.i0) {
