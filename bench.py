@@ -348,9 +348,9 @@ def run_ours(args):
     kname = {"fast-sym": "k_allpairs_sym", "fast": "k_allpairs_fast", "exact": "k_allpairs"}[args.precision]
     traffic, pipe, inst_prof = profiled_kernel(kname, n)
     # kernels of ours per step: count + scans + scatter + in-cell sort + pack (with the tie check) + pair kernel +
-    # partial sums + finish + unsort + rescan (fast-sym); sort (4) + pack + pair kernel + partition sums + unsort + rescan (fast); pack + pair
+    # partial sums + finish (in particle order) + rescan (fast-sym); sort (4) + pack + pair kernel + partition sums + unsort + rescan (fast); pack + pair
     # kernel (+ slot copy in / out when sharded) (exact); then the persistent step kernel
-    launches_per_step = {"fast-sym": 11, "fast": 10, "exact": 3 if world == 1 else 5}[args.precision]
+    launches_per_step = {"fast-sym": 10, "fast": 10, "exact": 3 if world == 1 else 5}[args.precision]
     inst = inst_prof or FP64_INST_PER_PAIR.get(args.precision)
     # roofline of the dominant kernel (the all-pairs pair kernel): the FP64 pipe.
     # achieved = the FP64 work the pair kernel executes per launch (FP64

@@ -123,7 +123,6 @@ struct SymWs {
     double* tval;    // (2 n) coordinates by bucket (x values, then y values)
     double* apart;   // (SY_S + 1, n, 2) receiver-side partial sums per chunk (+ the diagonal block)
     double* bpart;   // (D, n, 2) source-side partial sums per circulant distance
-    double* slot3;   // (n, 3) fx, fy, flag per slot
     double* part;    // (n, 2) P = A - B per slot (single GPU; ranks all-reduce their own)
 };
 
@@ -132,7 +131,7 @@ BD_HD int64_t sym_ws_bytes(int64_t n) {
     return fast_ws_bytes(n) + fs_align(16 * n) + 2 * fs_align(8 * n) + fs_align(64 * n) + fs_align(32 * sym_subs(n)) +
            fs_align(8 * sym_tiles(n)) + fs_align(4 * (2 * sym_tie_buckets(n) + 1)) +
            fs_align(8 * sym_tie_buckets(n)) + fs_align(16 * n) +
-           fs_align(16 * n * (SY_S + 1)) + fs_align(16 * n * D) + fs_align(24 * n) + fs_align(16 * n) + 256;
+           fs_align(16 * n * (SY_S + 1)) + fs_align(16 * n * D) + fs_align(16 * n) + 256;
 }
 
 BD_HD SymWs sym_ws_carve(void* base, int64_t n) {
@@ -151,7 +150,6 @@ BD_HD SymWs sym_ws_carve(void* base, int64_t n) {
     w.tval = (double*)b; b += fs_align(16 * n);
     w.apart = (double*)b; b += fs_align(16 * n * (SY_S + 1));
     w.bpart = (double*)b; b += fs_align(16 * n * D);
-    w.slot3 = (double*)b; b += fs_align(24 * n);
     w.part = (double*)b;
     return w;
 }
@@ -925,14 +923,16 @@ __global__ void k_sym_partial(int64_t n, SymWs w, SymRange g, double* __restrict
     }
 }
 
-// F = mu P per slot -> slot3 (fx, fy, flag)
-__global__ void k_sym_finish(int64_t n, SymWs w, const double* __restrict__ part) {
+// F = mu P per slot, written in particle order (out, err: 0, or -1 = re-scan exactly)
+__global__ void k_sym_finish(int64_t n, SymWs w, const double* __restrict__ part, double* __restrict__ out,
+                             int64_t* __restrict__ err) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         const double mu = w.smu[s];
         const double fx = mu * part[2 * s], fy = mu * part[2 * s + 1];
-        w.slot3[3 * s] = fx;
-        w.slot3[3 * s + 1] = fy;
-        w.slot3[3 * s + 2] = (isfinite(fx) && isfinite(fy)) ? 0.0 : -1.0;
+        const int64_t i = w.sort.order[s];
+        out[2 * i] = fx;
+        out[2 * i + 1] = fy;
+        err[i] = (isfinite(fx) && isfinite(fy)) ? 0 : -1;
     }
 }
 

@@ -696,8 +696,7 @@ int launch_sym_partial(const double* pos, const double* alpha, const double* mu,
 int launch_sym_finish(const double* pos, int64_t n, const bd_params_t& p, const SymWs& w, const double* part,
                       double* out, int64_t* err, cudaStream_t st) {
     if (n <= 0) return 0;
-    k_sym_finish<<<grid_for(n), 256, 0, st>>>(n, w, part);
-    k_unsort_forces<<<grid_for(n), 256, 0, st>>>(0, n, w.sort, w.slot3, out, err);
+    k_sym_finish<<<grid_for(n), 256, 0, st>>>(n, w, part, out, err);
     k_lr_rescan_pos<<<grid_for(n), 256, 0, st>>>(pos, n, p.L, p.mi_lo, p.mi_hi, err);
     return err_code(cudaGetLastError());
 }
