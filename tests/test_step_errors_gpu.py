@@ -10,10 +10,11 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("lr_c0_n256", "exact"), ("cfg1_lr_c0_n1024", "exact"), ("cfg1_lr_c0_n1024", "fast-sym")]
+CASES = [("lr_c0_n256", "exact"), ("cfg1_lr_c0_n1024", "exact"), ("cfg1_lr_c0_n1024", "fast-sym"),
+         ("lrsr_tri_n256", "exact")]
 
 
-@pytest.mark.parametrize("name,precision", CASES)
+@pytest.mark.parametrize("name,precision", CASES + [("sr_tri_n512", "exact")])
 def test_zero_separation_raises_singularity(name, precision):
     from golden_io import load
     from helpers import product_sim
