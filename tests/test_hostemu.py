@@ -258,3 +258,30 @@ def test_host_restore_delaunay_matches_reference_build(emu):
         assert emu.bdh_restore_delaunay(ctypes.byref(h.s), ctypes.byref(p)) >= 0
         for k in TRI_KEYS:
             assert np.array_equal(h.tri[k], b[f"{tag}_fin_{k}"]), (tag, k)
+
+
+@pytest.mark.parametrize("case", ["singular", "nonfinite"])
+def test_host_step_error_paths(emu, case):
+    """The fused check phase of the step driver (singularity, then
+    finiteness, with the rollback backup in the same phase): the status
+    and the offending indices of forces.py:54-58 / dynamics.py:84-86, and
+    an untouched state."""
+    from paper_1703_02484_b200._abi import BD_ERR_SINGULAR, BD_ERR_STEPFAIL
+    rec = load("lr_c0_n256")
+    p = params_for(emu, float(rec["L"]), int(rec["seed"]), float(rec["dt"]), float(rec["r_cutoff"]),
+                   n=int(rec["n"]), force_mode=0)
+    h = HostState(emu, rec, p)
+    if case == "singular":
+        h.pos[20] = h.pos[10]
+    else:
+        h.alpha[7] = np.nan
+    pos0 = h.pos.copy()
+    tri0 = {k: v.copy() for k, v in h.tri.items()}
+    st = BdStats()
+    emu.bdh_step_tri(ctypes.byref(h.s), ctypes.byref(p), ctypes.byref(st))
+    if case == "singular":
+        assert (st.status, st.err_i, st.err_k) == (BD_ERR_SINGULAR, 10, 20)
+    else:
+        assert st.status == BD_ERR_STEPFAIL and st.err_i == 0
+    assert np.array_equal(h.pos, pos0)
+    assert all(np.array_equal(h.tri[k], tri0[k]) for k in tri0)
